@@ -1,0 +1,30 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (CUDA device) and the built libbdeg.so")
+    config.addinivalue_line("markers", "slow: long-running CPU oracle case")
+
+
+def golden(name):
+    return os.path.join(ROOT, "tests", "golden", name)
+
+
+@pytest.fixture(scope="session")
+def table3():
+    out = {}
+    with open(golden("table3_degrees.txt")) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            m, k, v, kind = line.split()
+            out[(int(m), int(k))] = (int(v), kind)
+    return out
