@@ -1,0 +1,168 @@
+/* bdeg.h — C ABI of libbdeg.so: exact degree of the C*-solution set of a
+ * Laurent binomial system on NVIDIA B200 (sm_100a).
+ *
+ * Method: Chen & Mehta, arXiv 1501.02237.  The CPU front end
+ * computes the Smith Normal Form of the exponent matrix, which
+ * fixes the dimension d = n - rank A, the component count |prod d_j|
+ * (Prop. 1) and the parametrisation matrix P_0 (eq. rank-decomp).
+ * The degree of each component is the normalised volume
+ *     deg V = d! Vol_d(conv{p_0^(1), ..., p_0^(n), 0})      (Prop. 4)
+ * computed as the sum of |det| over the cells of the regular simplicial
+ * subdivision induced by a lifting omega: a (d+1)-subset is a
+ * cell iff the lower-face system I(a_0..a_d) (eq. lower-face) is
+ * (strictly) feasible.  The GPU enumerates every K-subset of the lifted
+ * point configuration by combinatorial rank (the brute force of P:798-800,
+ * made practical by prefix-shared fraction-free elimination).
+ *
+ * Conventions for every entry point:
+ *   - Nothing throws across the ABI; every call returns a bdeg_status.
+ *   - On error the output structs are left untouched; bdeg_last_error(plan)
+ *     (or bdeg_last_error(NULL) for errors before a plan exists) returns a
+ *     human-readable message valid until the next call on that plan.
+ *   - The caller owns every input array; bdeg_plan* copies what it needs.
+ *   - A plan is used by one host thread at a time; plans are independent.
+ *   - Device work is enqueued on options.stream (a cudaStream_t; NULL = the
+ *     legacy default stream) of options.device.
+ *   - There is NO CPU fallback: without a usable sm_100 device the device
+ *     entry points return BDEG_E_CUDA.
+ */
+#ifndef BDEG_H
+#define BDEG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bdeg_plan_s *bdeg_plan_t;
+
+typedef enum {
+    BDEG_OK = 0,
+    BDEG_E_INVALID = 1,       /* bad argument (shape, NULL pointer, range)            */
+    BDEG_E_INCONSISTENT = 2,  /* b^{Q_0} != 1: empty solution set         */
+    BDEG_E_DEGENERATE = 3,    /* lifting not generic ("almost all"); user-given
+                                 lifting, or max_relift generated liftings exhausted  */
+    BDEG_E_IO = 4,            /* reserved (SPEC exit code 4)                           */
+    BDEG_E_TOO_LARGE = 5,     /* N > 64, K > 32, or an exact value exceeds int64       */
+    BDEG_E_CUDA = 6,          /* CUDA runtime error / no sm_100 device                 */
+    BDEG_E_COMM = 7           /* reserved for the multi-GPU combine                    */
+} bdeg_status;
+
+/* x^A = b (eq. standard-form). */
+typedef struct {
+    int32_t n;               /* number of variables (rows of A), n >= 1              */
+    int32_t m;               /* number of binomials (columns of A), m >= 0           */
+    const int64_t *A;        /* n*m, ROW-major: A[i*m + j]; column j = alpha_j - beta_j */
+    const double *b_re;      /* m entries (real part of b_j = -c_{j,2}/c_{j,1}), or NULL => b = 1 */
+    const double *b_im;      /* m entries or NULL (=> imaginary parts 0)             */
+    const int64_t *lifting;  /* n+1 values: omega per variable, last = the origin;
+                                NULL => generated from options.seed (SplitMix64,
+                                values in [0, 2^lift_bits)).            */
+} bdeg_problem;
+
+/* options.flags */
+#define BDEG_FLAG_NO_LLL            0x1u  /* keep the SNF basis of P_0 (no LLL reduction)     */
+#define BDEG_FLAG_NO_HOMOG_SHORTCUT 0x2u  /* always K = d+1 with the origin (no pyramid K = d)  */
+#define BDEG_FLAG_FORCE_TIER0       0x4u  /* start in the int32 tier even if the planner would not */
+#define BDEG_FLAG_FORCE_TIER1       0x8u  /* skip the int32 tier                                  */
+#define BDEG_FLAG_NO_RELIFT         0x10u /* report BDEG_E_DEGENERATE instead of re-lifting       */
+
+typedef struct {
+    uint64_t seed;           /* seed of the generated lifting (and of re-lifts)      */
+    int32_t lift_bits;       /* generated omega in [0, 2^lift_bits); default 20      */
+    int32_t max_relift;      /* re-lift attempts for generated liftings; default 32  */
+    int32_t device;          /* CUDA device ordinal; default 0                       */
+    int32_t rank, world;     /* this process's shard of rank space (default 0, 1)    */
+    void *stream;            /* cudaStream_t for every launch/copy; NULL = default   */
+    uint32_t flags;          /* BDEG_FLAG_*                                          */
+    int32_t inner_levels;    /* register-resident DFS depth S in 0..3; -1 = auto     */
+    int32_t ctas_per_sm;     /* persistent CTAs per SM; 0 = auto                     */
+} bdeg_options;
+
+typedef struct {
+    /* front end (bdeg_plan / bdeg_plan_info) */
+    int32_t n, rank, dim;    /* dim = n - rank (Prop. 1)                             */
+    int32_t K, N;            /* subset size and number of lifted points              */
+    int32_t tier;            /* arithmetic tier the enumeration started in (0 or 1)  */
+    int32_t homogeneous;     /* 1 if 1^T A = 0 (K = d, pyramid reading)              */
+    int32_t inner_levels;    /* S used by the kernel                                 */
+    uint64_t comp_lo, comp_hi;        /* |prod d_j| as unsigned 128-bit      */
+    /* enumeration (bdeg_degree / bdeg_finalize) */
+    uint64_t deg_lo; int64_t deg_hi;  /* degree of each component, signed 128-bit    */
+    uint64_t candidates;     /* K-subsets examined (= C(N,K) for a full run)         */
+    uint64_t cells;          /* cells of the regular subdivision (lifting-dependent) */
+    uint64_t singular;       /* K-subsets with det = 0 (lifting-independent)         */
+    uint64_t ties;           /* would-be cells with a zero facet value (degenerate)  */
+    uint64_t overflow_reruns;/* blocks re-run in the int64 tier                      */
+    uint64_t updates;        /* fraction-free elimination updates executed          */
+    uint64_t leaves;         /* (K-1)-prefixes tested (each = one warp-wide facet test) */
+    int32_t relifts;         /* re-lift attempts used                                */
+    int32_t consistent;      /* 0 if b^{Q_0} != 1                                    */
+    uint64_t seed_used;      /* seed of the lifting that produced the result         */
+    uint64_t total_candidates; /* C(N,K)                                             */
+    double plan_ms, kernel_ms, total_ms;
+} bdeg_result;
+
+#define BDEG_NSLOTS 16       /* int64 partial-result slots combined by one all-reduce(SUM) */
+
+/* Fill *o with the defaults listed above. */
+void bdeg_default_options(bdeg_options *o);
+
+/* Front end + planner (CPU) for x^A = b.  Copies the inputs.  Returns
+ * BDEG_E_INCONSISTENT for an empty solution set, BDEG_E_TOO_LARGE when the
+ * point configuration exceeds N <= 64, K <= 32, BDEG_E_INVALID on bad
+ * shapes.  d = 0 plans are valid (degree 1, no device work). */
+bdeg_status bdeg_plan(const bdeg_problem *prob, const bdeg_options *opt, bdeg_plan_t *out);
+
+/* Plan directly on a lifted vector configuration: K-vectors V (N*K,
+ * POINT-major, V[l*K + t]) with lifting (N values, or NULL => generated).
+ * Cells are K-subsets sigma with sign det[[V_sig, v_l],[w_sig, w_l]] =
+ * sign det V_sig for every other l (lower facets of the lifted cone).  For an
+ * affine point set a_l in Z^{K-1} pass v_l = (1, a_l). */
+bdeg_status bdeg_plan_points(int32_t K, int32_t N, const int64_t *V, const int64_t *lifting,
+                             const bdeg_options *opt, bdeg_plan_t *out);
+
+/* Front-end fields of the result (no device work). */
+bdeg_status bdeg_plan_info(bdeg_plan_t plan, bdeg_result *out);
+
+/* Device workspace: bytes needed, and an optional caller-owned device buffer
+ * (e.g. a torch.uint8 CUDA tensor) that must outlive the plan's device work.
+ * Without it the plan allocates with cudaMalloc on first use. */
+size_t bdeg_workspace_bytes(bdeg_plan_t plan);
+bdeg_status bdeg_set_workspace(bdeg_plan_t plan, void *d_ptr, size_t bytes);
+
+/* Whole rank space on one GPU, synchronous (returns after the D2H read of
+ * the result).  Handles overflow re-runs and, for generated liftings,
+ * re-lifts on degeneracy.  BDEG_E_DEGENERATE for a degenerate user lifting. */
+bdeg_status bdeg_degree(bdeg_plan_t plan, bdeg_result *out);
+
+/* Same over the colex ranks [begin, end) of K-subsets (rank = sum_i
+ * C(c_i, i+1), c_0 < ... < c_{K-1}); no re-lift (ties are reported). */
+bdeg_status bdeg_degree_range(bdeg_plan_t plan, uint64_t begin, uint64_t end, bdeg_result *out);
+
+/* This process's shard (options.rank of options.world) accumulated into the
+ * caller's DEVICE buffer d_slots (BDEG_NSLOTS int64, zeroed here), async on
+ * the stream.  Combine with one all-reduce(SUM) and call bdeg_finalize. */
+bdeg_status bdeg_degree_partial(bdeg_plan_t plan, int64_t *d_slots);
+
+/* Carry-normalise summed slots (HOST memory) into *out. */
+bdeg_status bdeg_finalize(bdeg_plan_t plan, const int64_t *h_slots, bdeg_result *out);
+
+/* Replace a generated lifting with the one for re-lift attempt `attempt`
+ * (seed derived from options.seed); BDEG_E_INVALID for a user lifting. */
+bdeg_status bdeg_relift(bdeg_plan_t plan, int32_t attempt);
+
+const char *bdeg_last_error(bdeg_plan_t plan);
+const char *bdeg_status_str(bdeg_status s);
+void bdeg_destroy(bdeg_plan_t plan);
+
+/* Number of kernels this process has launched through libbdeg (evidence for
+ * bench.py's gpu_launches). */
+uint64_t bdeg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BDEG_H */

@@ -1,0 +1,329 @@
+"""Thin ctypes binding of libbdeg.so (include/bdeg.h) — argument marshalling
+only.  Every step of the degree computation runs in the library: the C++
+front end (Smith form, P_0, point configuration, planner) and the sm_100a
+kernels.  There is no Python or CPU fallback: if libbdeg.so is missing the
+import fails, and device entry points raise BdegError(BDEG_E_CUDA) without
+a B200.
+
+PyTorch is used only as plumbing: device workspace (a torch.uint8 CUDA
+tensor), the current CUDA stream, and torch.distributed for the multi-GPU
+all-reduce (see bench.py / multi.py).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbdeg.so")
+
+BDEG_OK = 0
+BDEG_E_INVALID = 1
+BDEG_E_INCONSISTENT = 2
+BDEG_E_DEGENERATE = 3
+BDEG_E_IO = 4
+BDEG_E_TOO_LARGE = 5
+BDEG_E_CUDA = 6
+BDEG_E_COMM = 7
+
+FLAG_NO_LLL = 0x1
+FLAG_NO_HOMOG_SHORTCUT = 0x2
+FLAG_FORCE_TIER0 = 0x4
+FLAG_FORCE_TIER1 = 0x8
+FLAG_NO_RELIFT = 0x10
+
+NSLOTS = 16
+
+
+class BdegError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"bdeg error {status}: {msg}")
+        self.status = status
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("m", ctypes.c_int32),
+                ("A", ctypes.POINTER(ctypes.c_int64)),
+                ("b_re", ctypes.POINTER(ctypes.c_double)),
+                ("b_im", ctypes.POINTER(ctypes.c_double)),
+                ("lifting", ctypes.POINTER(ctypes.c_int64))]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("lift_bits", ctypes.c_int32),
+                ("max_relift", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("stream", ctypes.c_void_p), ("flags", ctypes.c_uint32),
+                ("inner_levels", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32)]
+
+
+class _Result(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("rank", ctypes.c_int32), ("dim", ctypes.c_int32),
+                ("K", ctypes.c_int32), ("N", ctypes.c_int32), ("tier", ctypes.c_int32),
+                ("homogeneous", ctypes.c_int32), ("inner_levels", ctypes.c_int32),
+                ("comp_lo", ctypes.c_uint64), ("comp_hi", ctypes.c_uint64),
+                ("deg_lo", ctypes.c_uint64), ("deg_hi", ctypes.c_int64),
+                ("candidates", ctypes.c_uint64), ("cells", ctypes.c_uint64),
+                ("singular", ctypes.c_uint64), ("ties", ctypes.c_uint64),
+                ("overflow_reruns", ctypes.c_uint64), ("updates", ctypes.c_uint64),
+                ("leaves", ctypes.c_uint64), ("relifts", ctypes.c_int32),
+                ("consistent", ctypes.c_int32), ("seed_used", ctypes.c_uint64),
+                ("total_candidates", ctypes.c_uint64),
+                ("plan_ms", ctypes.c_double), ("kernel_ms", ctypes.c_double),
+                ("total_ms", ctypes.c_double)]
+
+
+EXPORTS = ["bdeg_default_options", "bdeg_plan", "bdeg_plan_points", "bdeg_plan_info",
+           "bdeg_workspace_bytes", "bdeg_set_workspace", "bdeg_degree", "bdeg_degree_range",
+           "bdeg_degree_partial", "bdeg_finalize", "bdeg_relift", "bdeg_last_error",
+           "bdeg_status_str", "bdeg_destroy", "bdeg_launch_count"]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(libbdeg has no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    plan_t = ctypes.c_void_p
+    lib.bdeg_default_options.argtypes = [P(_Options)]
+    lib.bdeg_default_options.restype = None
+    lib.bdeg_plan.argtypes = [P(_Problem), P(_Options), P(plan_t)]
+    lib.bdeg_plan_points.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int64),
+                                     P(ctypes.c_int64), P(_Options), P(plan_t)]
+    lib.bdeg_plan_info.argtypes = [plan_t, P(_Result)]
+    lib.bdeg_workspace_bytes.argtypes = [plan_t]
+    lib.bdeg_workspace_bytes.restype = ctypes.c_size_t
+    lib.bdeg_set_workspace.argtypes = [plan_t, ctypes.c_void_p, ctypes.c_size_t]
+    lib.bdeg_degree.argtypes = [plan_t, P(_Result)]
+    lib.bdeg_degree_range.argtypes = [plan_t, ctypes.c_uint64, ctypes.c_uint64, P(_Result)]
+    lib.bdeg_degree_partial.argtypes = [plan_t, ctypes.c_void_p]
+    lib.bdeg_finalize.argtypes = [plan_t, P(ctypes.c_int64), P(_Result)]
+    lib.bdeg_relift.argtypes = [plan_t, ctypes.c_int32]
+    lib.bdeg_last_error.argtypes = [plan_t]
+    lib.bdeg_last_error.restype = ctypes.c_char_p
+    lib.bdeg_status_str.argtypes = [ctypes.c_int]
+    lib.bdeg_status_str.restype = ctypes.c_char_p
+    lib.bdeg_destroy.argtypes = [plan_t]
+    lib.bdeg_destroy.restype = None
+    lib.bdeg_launch_count.argtypes = []
+    lib.bdeg_launch_count.restype = ctypes.c_uint64
+    for name in ["bdeg_plan", "bdeg_plan_points", "bdeg_plan_info", "bdeg_set_workspace",
+                 "bdeg_degree", "bdeg_degree_range", "bdeg_degree_partial", "bdeg_finalize",
+                 "bdeg_relift"]:
+        getattr(lib, name).restype = ctypes.c_int
+    return lib
+
+
+lib = _load()
+
+
+def launch_count() -> int:
+    return int(lib.bdeg_launch_count())
+
+
+@dataclass
+class Result:
+    n: int
+    rank: int
+    dim: int
+    K: int
+    N: int
+    tier: int
+    homogeneous: bool
+    inner_levels: int
+    components: int
+    degree: int
+    candidates: int
+    cells: int
+    singular: int
+    ties: int
+    overflow_reruns: int
+    updates: int
+    leaves: int
+    relifts: int
+    consistent: bool
+    seed_used: int
+    total_candidates: int
+    plan_ms: float
+    kernel_ms: float
+    total_ms: float
+    extra: dict = field(default_factory=dict)
+
+
+def _result(r: _Result) -> Result:
+    deg = (r.deg_hi << 64) | r.deg_lo
+    comps = (r.comp_hi << 64) | r.comp_lo
+    return Result(n=r.n, rank=r.rank, dim=r.dim, K=r.K, N=r.N, tier=r.tier,
+                  homogeneous=bool(r.homogeneous), inner_levels=r.inner_levels,
+                  components=comps, degree=deg, candidates=r.candidates, cells=r.cells,
+                  singular=r.singular, ties=r.ties, overflow_reruns=r.overflow_reruns,
+                  updates=r.updates, leaves=r.leaves, relifts=r.relifts,
+                  consistent=bool(r.consistent), seed_used=r.seed_used,
+                  total_candidates=r.total_candidates, plan_ms=r.plan_ms,
+                  kernel_ms=r.kernel_ms, total_ms=r.total_ms)
+
+
+def _options(seed=1, lift_bits=20, max_relift=32, device=0, rank=0, world=1, stream=None,
+             flags=0, inner_levels=-1, ctas_per_sm=0) -> _Options:
+    o = _Options()
+    lib.bdeg_default_options(ctypes.byref(o))
+    o.seed = seed & ((1 << 64) - 1)
+    o.lift_bits = lift_bits
+    o.max_relift = max_relift
+    o.device = device
+    o.rank = rank
+    o.world = world
+    o.stream = stream
+    o.flags = flags
+    o.inner_levels = inner_levels
+    o.ctas_per_sm = ctas_per_sm
+    return o
+
+
+def _i64(values):
+    vals = [int(v) for v in values]
+    return (ctypes.c_int64 * max(1, len(vals)))(*vals)
+
+
+def _check(status, plan=None):
+    if status != BDEG_OK:
+        msg = lib.bdeg_last_error(plan).decode(errors="replace")
+        raise BdegError(status, msg)
+
+
+def _current_stream():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream).value
+    except Exception:  # noqa: BLE001 - torch is plumbing only
+        pass
+    return None
+
+
+class Plan:
+    """A planned degree computation (one bdeg_plan_t)."""
+
+    def __init__(self, handle, keep):
+        self._h = handle
+        self._keep = keep
+        self._ws = None
+
+    # -- construction ------------------------------------------------
+    @classmethod
+    def from_system(cls, A, b=None, lifting=None, **opts):
+        """x^A = b with A given as n rows of m ints."""
+        n = len(A)
+        m = len(A[0]) if n else 0
+        if "stream" not in opts:
+            opts["stream"] = _current_stream()
+        pr = _Problem()
+        pr.n, pr.m = n, m
+        Abuf = _i64([A[i][j] for i in range(n) for j in range(m)])
+        pr.A = Abuf
+        keep = [Abuf]
+        if b is not None:
+            bre = (ctypes.c_double * max(1, m))(*[complex(x).real for x in b])
+            bim = (ctypes.c_double * max(1, m))(*[complex(x).imag for x in b])
+            pr.b_re, pr.b_im = bre, bim
+            keep += [bre, bim]
+        if lifting is not None:
+            if len(lifting) != n + 1:
+                raise ValueError("lifting needs n+1 values (variables, then the origin)")
+            lb = _i64(lifting)
+            pr.lifting = lb
+            keep.append(lb)
+        o = _options(**opts)
+        h = ctypes.c_void_p()
+        _check(lib.bdeg_plan(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(h)))
+        return cls(h, keep)
+
+    @classmethod
+    def from_points(cls, V, lifting=None, **opts):
+        """Lifted vector configuration: N K-vectors (point-major)."""
+        N = len(V)
+        K = len(V[0])
+        if "stream" not in opts:
+            opts["stream"] = _current_stream()
+        Vb = _i64([x for v in V for x in v])
+        lb = _i64(lifting) if lifting is not None else None
+        o = _options(**opts)
+        h = ctypes.c_void_p()
+        _check(lib.bdeg_plan_points(K, N, Vb, lb, ctypes.byref(o), ctypes.byref(h)))
+        return cls(h, [Vb, lb])
+
+    # -- queries -----------------------------------------------------
+    def info(self) -> Result:
+        r = _Result()
+        _check(lib.bdeg_plan_info(self._h, ctypes.byref(r)), self._h)
+        return _result(r)
+
+    def workspace_bytes(self) -> int:
+        return int(lib.bdeg_workspace_bytes(self._h))
+
+    def use_torch_workspace(self, device=None):
+        """Give the plan a torch-allocated device workspace (PyTorch memory)."""
+        import torch
+        nbytes = self.workspace_bytes()
+        if nbytes == 0:
+            return None
+        dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+        ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
+        ptr = ws.data_ptr()
+        aligned = (ptr + 255) & ~255
+        _check(lib.bdeg_set_workspace(self._h, ctypes.c_void_p(aligned), nbytes), self._h)
+        self._ws = ws
+        return ws
+
+    def degree(self) -> Result:
+        r = _Result()
+        _check(lib.bdeg_degree(self._h, ctypes.byref(r)), self._h)
+        return _result(r)
+
+    def degree_range(self, begin: int, end: int) -> Result:
+        r = _Result()
+        _check(lib.bdeg_degree_range(self._h, begin, end, ctypes.byref(r)), self._h)
+        return _result(r)
+
+    def degree_partial(self, d_slots_ptr: int):
+        """Enqueue this rank's shard into a device int64[16] buffer (pointer)."""
+        _check(lib.bdeg_degree_partial(self._h, ctypes.c_void_p(d_slots_ptr)), self._h)
+
+    def finalize(self, h_slots) -> Result:
+        buf = _i64(h_slots)
+        r = _Result()
+        _check(lib.bdeg_finalize(self._h, buf, ctypes.byref(r)), self._h)
+        return _result(r)
+
+    def relift(self, attempt: int):
+        _check(lib.bdeg_relift(self._h, attempt), self._h)
+
+    def close(self):
+        if self._h:
+            lib.bdeg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def degree(A, b=None, lifting=None, **opts) -> Result:
+    """deg of each component of V*(x^A - b) (Prop. 4) on the GPU."""
+    with Plan.from_system(A, b, lifting, **opts) as p:
+        return p.degree()
+
+
+def degree_points(V, lifting=None, **opts) -> Result:
+    with Plan.from_points(V, lifting, **opts) as p:
+        return p.degree()

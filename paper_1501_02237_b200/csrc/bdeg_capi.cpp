@@ -1,0 +1,609 @@
+// extern "C" boundary of libbdeg.so (include/bdeg.h): planning, device
+// workspace, launches, overflow re-runs, re-lifting and the exact combine.
+#include "../../include/bdeg.h"
+#include "bdeg_internal.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace bdeg;
+
+struct bdeg_plan_s {
+    // inputs
+    bool points_mode = false;
+    int n = 0, m = 0;
+    std::vector<int64_t> A;
+    std::vector<double> bre, bim;
+    bool user_lift = false;
+    std::vector<int64_t> lift;        // n+1 (system) or N (points) values in use
+    bdeg_options opt{};
+    // front end
+    FrontEnd fe;
+    int K = 0, N = 0, origin_index = -1;
+    std::vector<int64_t> V, w;        // point-major N x K, and N lifts
+    std::vector<int> point_of_var;
+    int tier = 0, S = 0, T = 0;
+    uint64_t nblocks = 0, total = 0;
+    uint64_t seed_used = 0;
+    int relifts = 0;
+    double plan_ms = 0;
+    std::string err;
+    // device
+    bool dev_ready = false, own_ws = false, l_dirty = true;
+    char *ws = nullptr;
+    size_t ws_bytes = 0;
+    unsigned long long *d_slots = nullptr, *d_ctr = nullptr, *d_ovfq = nullptr;
+    int64_t *d_L = nullptr;
+    uint64_t *d_B = nullptr;
+    uint64_t ovf_cap = 1 << 16;
+    int grid = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<uint64_t> binom;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+bdeg_status fail(bdeg_plan_t p, bdeg_status s, const std::string &msg) {
+    if (p) p->err = msg;
+    g_err = msg;
+    return s;
+}
+
+uint64_t C(const std::vector<uint64_t> &B, int n, int k) {
+    if (n < 0 || k < 0 || k > n) return 0;
+    return B[(size_t)n * kBinomCols + k];
+}
+
+void fill_binom(std::vector<uint64_t> &B) {
+    B.assign((size_t)kBinomRows * kBinomCols, 0);
+    for (int n = 0; n < kBinomRows; ++n) {
+        B[(size_t)n * kBinomCols] = 1;
+        for (int k = 1; k < kBinomCols && k <= n; ++k)
+            B[(size_t)n * kBinomCols + k] = B[(size_t)(n - 1) * kBinomCols + k - 1] +
+                                            (k <= n - 1 ? B[(size_t)(n - 1) * kBinomCols + k] : 0);
+    }
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// workspace layout
+struct Layout {
+    size_t slots, ctr, L, B, q, total;
+};
+Layout layout(const bdeg_plan_s *p) {
+    Layout l;
+    size_t off = 0;
+    l.slots = off; off = align256(off + kNSlots * 8);
+    l.ctr = off;   off = align256(off + 8 * 8);
+    l.L = off;     off = align256(off + (((size_t)(p->K + 1) * p->N * 8 + 15) & ~(size_t)15));
+    l.B = off;     off = align256(off + (size_t)kBinomRows * kBinomCols * 8);
+    l.q = off;     off = align256(off + p->ovf_cap * 8);
+    l.total = off;
+    return l;
+}
+
+void gen_lifting(uint64_t seed, int count, int bits, std::vector<int64_t> &out) {
+    SplitMix64 g(seed);
+    out.resize(count);
+    const int sh = 64 - std::max(1, std::min(bits, 62));
+    for (int i = 0; i < count; ++i) out[i] = (int64_t)(g.next() >> sh);
+}
+
+// colex unrank (host planner)
+void unrank(const std::vector<uint64_t> &B, uint64_t r, int K, std::vector<int> &c) {
+    c.assign(K, 0);
+    for (int i = K - 1; i >= 0; --i) {
+        int x = i;
+        while (C(B, x + 1, i + 1) <= r) ++x;
+        c[i] = x;
+        r -= C(B, x, i + 1);
+    }
+}
+
+uint64_t block_of(const bdeg_plan_s *p, uint64_t rank) {
+    if (p->T == 0) return 0;
+    std::vector<int> c;
+    unrank(p->binom, rank, p->K, c);
+    uint64_t b = 0;
+    for (int t = 0; t < p->T; ++t) b += C(p->binom, c[p->S + 1 + t] - p->S - 1, t + 1);
+    return b;
+}
+
+// Largest magnitude (bits) of the fraction-free elimination values along a
+// few sampled prefixes — steers the choice of the starting tier only (the
+// kernel checks every value anyway).
+int sample_bits(const bdeg_plan_s *p) {
+    const int K = p->K, N = p->N;
+    SplitMix64 g(0x5eed ^ p->seed_used);
+    i128 mx = 1;
+    for (int s = 0; s < 96; ++s) {
+        std::vector<int> perm(N);
+        for (int i = 0; i < N; ++i) perm[i] = i;
+        for (int i = N - 1; i > 0; --i) std::swap(perm[i], perm[g.next() % (uint64_t)(i + 1)]);
+        std::vector<std::vector<i128>> M(K + 1, std::vector<i128>(N));
+        for (int l = 0; l < N; ++l) {
+            for (int i = 0; i < K; ++i) M[i][l] = p->V[(size_t)l * K + i];
+            M[K][l] = p->w[l];
+        }
+        std::vector<char> alive(K, 1);
+        i128 prev = 1;
+        for (int t = 0; t < K - 1; ++t) {
+            const int piv_c = perm[t];
+            int r = -1;
+            for (int i = 0; i < K; ++i) if (alive[i] && M[i][piv_c] != 0) { r = i; break; }
+            if (r < 0) break;
+            const i128 piv = M[r][piv_c];
+            bool big = false;
+            for (int i = 0; i <= K && !big; ++i) {
+                if (i == r || (i < K && !alive[i])) continue;
+                const i128 ci = M[i][piv_c];
+                for (int l = 0; l < N; ++l) {
+                    i128 a, b2;
+                    if (__builtin_mul_overflow(piv, M[i][l], &a) || __builtin_mul_overflow(ci, M[r][l], &b2)) { big = true; break; }
+                    M[i][l] = (a - b2) / prev;
+                    i128 v = M[i][l] < 0 ? -M[i][l] : M[i][l];
+                    if (v > mx) mx = v;
+                }
+            }
+            if (big) return 127;
+            alive[r] = 0;
+            prev = piv;
+        }
+    }
+    int bits = 0;
+    while (mx > 0) { ++bits; mx >>= 1; }
+    return bits;
+}
+
+void choose_tier_and_blocks(bdeg_plan_s *p) {
+    p->total = C(p->binom, p->N, p->K);
+    const int bits = sample_bits(p);
+    p->tier = (bits <= 26) ? 0 : 1;
+    if (p->opt.flags & BDEG_FLAG_FORCE_TIER0) p->tier = 0;
+    if (p->opt.flags & BDEG_FLAG_FORCE_TIER1) p->tier = 1;
+    const int smax = std::min(3, p->K - 1);
+    int S = -1;
+    if (p->opt.inner_levels >= 0) {
+        S = std::min(p->opt.inner_levels, smax);
+    } else {
+        const uint64_t target = 1u << 16;
+        for (int s = smax; s >= 0; --s)
+            if (C(p->binom, p->N - s - 1, p->K - 1 - s) >= target) { S = s; break; }
+        if (S < 0) {   // small problem: maximise the number of blocks
+            uint64_t best = 0;
+            for (int s = 0; s <= smax; ++s) {
+                const uint64_t nb = C(p->binom, p->N - s - 1, p->K - 1 - s);
+                if (nb > best) { best = nb; S = s; }
+            }
+        }
+    }
+    p->S = std::max(S, 0);
+    p->T = p->K - 1 - p->S;
+    p->nblocks = C(p->binom, p->N - p->S - 1, p->T);
+}
+
+bdeg_status finish_plan(bdeg_plan_s *p) {
+    if (p->K > kMaxK || p->N > kMaxN)
+        return fail(p, BDEG_E_TOO_LARGE, "point configuration exceeds N <= 64, K <= 32 (N=" +
+                                              std::to_string(p->N) + ", K=" + std::to_string(p->K) + ")");
+    for (int64_t v : p->V)
+        if (v > ((int64_t)1 << 40) || v < -((int64_t)1 << 40))
+            return fail(p, BDEG_E_TOO_LARGE, "point coordinate beyond 2^40");
+    for (int64_t v : p->w)
+        if (v > ((int64_t)1 << 52) || v < -((int64_t)1 << 52))
+            return fail(p, BDEG_E_TOO_LARGE, "lifting value beyond 2^52");
+    choose_tier_and_blocks(p);
+    p->l_dirty = true;
+    return BDEG_OK;
+}
+
+// rebuild V/w from the current lifting (system plans)
+void rebuild_points(bdeg_plan_s *p) {
+    build_points(p->fe, p->lift.data(), !(p->opt.flags & BDEG_FLAG_NO_HOMOG_SHORTCUT), p->K, p->N, p->V,
+                 p->w, p->point_of_var, p->origin_index);
+}
+
+bdeg_status ensure_device(bdeg_plan_s *p) {
+    cudaError_t e;
+    if (!p->dev_ready) {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= p->opt.device)
+            return fail(p, BDEG_E_CUDA, "no CUDA device available (libbdeg has no CPU fallback)");
+        if ((e = cudaSetDevice(p->opt.device)) != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
+        cudaDeviceProp prop;
+        cudaGetDeviceProperties(&prop, p->opt.device);
+        if (prop.major < 10) return fail(p, BDEG_E_CUDA, "libbdeg is built for sm_100a (B200); device is older");
+        const Layout L = layout(p);
+        if (!p->ws) {
+            if ((e = cudaMalloc(&p->ws, L.total)) != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
+            p->own_ws = true;
+            p->ws_bytes = L.total;
+        } else if (p->ws_bytes < L.total) {
+            return fail(p, BDEG_E_INVALID, "workspace too small");
+        }
+        p->d_slots = reinterpret_cast<unsigned long long *>(p->ws + L.slots);
+        p->d_ctr = reinterpret_cast<unsigned long long *>(p->ws + L.ctr);
+        p->d_L = reinterpret_cast<int64_t *>(p->ws + L.L);
+        p->d_B = reinterpret_cast<uint64_t *>(p->ws + L.B);
+        p->d_ovfq = reinterpret_cast<unsigned long long *>(p->ws + L.q);
+        cudaStream_t st = (cudaStream_t)p->opt.stream;
+        if ((e = cudaMemcpyAsync(p->d_B, p->binom.data(), p->binom.size() * 8, cudaMemcpyHostToDevice, st)) !=
+            cudaSuccess)
+            return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
+        cudaEventCreate(&p->ev0);
+        cudaEventCreate(&p->ev1);
+        LaunchArgs a{};
+        a.P.K = p->K; a.P.N = p->N; a.P.S = p->S; a.P.T = p->T;
+        a.tier = p->tier;
+        const int occ = std::max(enumerate_max_ctas_per_sm(a), 1);
+        const int per_sm = p->opt.ctas_per_sm > 0 ? std::min(p->opt.ctas_per_sm, occ) : occ;
+        p->grid = prop.multiProcessorCount * per_sm;
+        p->dev_ready = true;
+    }
+    if (p->l_dirty) {
+        // lifted matrix, column-major (K+1) x N, padded to 16 bytes
+        std::vector<int64_t> Lh((size_t)(p->K + 1) * p->N + 2, 0);
+        for (int l = 0; l < p->N; ++l) {
+            for (int i = 0; i < p->K; ++i) Lh[(size_t)l * (p->K + 1) + i] = p->V[(size_t)l * p->K + i];
+            Lh[(size_t)l * (p->K + 1) + p->K] = p->w[l];
+        }
+        const size_t bytes = (((size_t)(p->K + 1) * p->N * 8 + 15) & ~(size_t)15);
+        if ((e = cudaMemcpyAsync(p->d_L, Lh.data(), bytes, cudaMemcpyHostToDevice, (cudaStream_t)p->opt.stream)) !=
+            cudaSuccess)
+            return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
+        // pageable source: make sure the copy has consumed Lh before it dies
+        cudaStreamSynchronize((cudaStream_t)p->opt.stream);
+        p->l_dirty = false;
+    }
+    return BDEG_OK;
+}
+
+// Enqueue the enumeration of ranks [b, e) (this rank's interleaved share of
+// blocks) accumulating into `slots` (zeroed here).
+bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long long *slots, int rank,
+                          int world, int force_tier) {
+    cudaStream_t st = (cudaStream_t)p->opt.stream;
+    cudaError_t ce;
+    if ((ce = cudaMemsetAsync(slots, 0, kNSlots * 8, st)) != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+    if ((ce = cudaMemsetAsync(p->d_ctr, 0, 8 * 8, st)) != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+    if (e > p->total) e = p->total;
+    if (b >= e) return BDEG_OK;
+    LaunchArgs a{};
+    a.P.L = p->d_L;
+    a.P.binom = p->d_B;
+    a.P.K = p->K; a.P.N = p->N; a.P.S = p->S; a.P.T = p->T;
+    a.rank_begin = b;
+    a.rank_end = e;
+    a.blk_first = block_of(p, b);
+    a.blk_last = block_of(p, e - 1);
+    a.blk_offset = (uint64_t)rank;
+    a.blk_stride = (uint64_t)std::max(world, 1);
+    a.slots = slots;
+    a.ovf_queue = p->d_ovfq;
+    a.ovf_count = p->d_ctr + 2;
+    a.ovf_cap = p->ovf_cap;
+    a.grid = p->grid;
+    a.stream = st;
+    a.tier = force_tier >= 0 ? force_tier : p->tier;
+    a.replay = 0;
+    a.counter = p->d_ctr + 0;
+    int rc = launch_enumerate(a);
+    if (rc) return fail(p, BDEG_E_CUDA, std::string("k_enumerate launch: ") + cudaGetErrorString((cudaError_t)rc));
+    if (a.tier == 0) {   // re-run the blocks that left the int32 tier, in int64
+        a.tier = 1;
+        a.replay = 1;
+        a.counter = p->d_ctr + 1;
+        rc = launch_enumerate(a);
+        if (rc) return fail(p, BDEG_E_CUDA, std::string("k_enumerate replay: ") + cudaGetErrorString((cudaError_t)rc));
+    }
+    return BDEG_OK;
+}
+
+void fill_front(const bdeg_plan_s *p, bdeg_result *r) {
+    std::memset(r, 0, sizeof(*r));
+    r->n = p->points_mode ? p->N : p->fe.n;
+    r->rank = p->points_mode ? 0 : p->fe.rank;
+    r->dim = p->points_mode ? p->K - 1 : p->fe.dim;
+    r->K = p->K;
+    r->N = p->N;
+    r->tier = p->tier;
+    r->homogeneous = p->points_mode ? 0 : (p->fe.homogeneous && !(p->opt.flags & BDEG_FLAG_NO_HOMOG_SHORTCUT));
+    r->inner_levels = p->S;
+    r->comp_lo = p->points_mode ? 1 : (uint64_t)p->fe.components;
+    r->comp_hi = p->points_mode ? 0 : (uint64_t)(p->fe.components >> 64);
+    r->consistent = p->points_mode ? 1 : p->fe.consistent;
+    r->seed_used = p->seed_used;
+    r->relifts = p->relifts;
+    r->total_candidates = p->total;
+    r->plan_ms = p->plan_ms;
+}
+
+bdeg_status slots_to_result(bdeg_plan_s *p, const int64_t *h, bdeg_result *r) {
+    if (h[SLOT_FATAL] > 0)
+        return fail(p, BDEG_E_TOO_LARGE, "an exact elimination value exceeded the int64 tier (|v| >= 2^62)");
+    u128 vol = 0;
+    for (int i = 3; i >= 0; --i) vol = (vol << 32) + (u128)(uint64_t)h[SLOT_VOL0 + i];
+    r->deg_lo = (uint64_t)vol;
+    r->deg_hi = (int64_t)(uint64_t)(vol >> 64);
+    r->cells = (uint64_t)h[SLOT_CELLS];
+    r->singular = (uint64_t)h[SLOT_SINGULAR];
+    r->candidates = (uint64_t)h[SLOT_CAND];
+    r->ties = (uint64_t)h[SLOT_TIES];
+    r->overflow_reruns = (uint64_t)h[SLOT_OVF_BLOCKS];
+    r->updates = (uint64_t)h[SLOT_UPDATES];
+    r->leaves = (uint64_t)h[SLOT_LEAVES];
+    return BDEG_OK;
+}
+
+// one synchronous pass over [b, e) on this GPU; re-runs everything in the
+// int64 tier if the overflow queue was exhausted.
+bdeg_status run_sync(bdeg_plan_s *p, uint64_t b, uint64_t e, int64_t *h, double *kms) {
+    cudaStream_t st = (cudaStream_t)p->opt.stream;
+    bdeg_status s = ensure_device(p);
+    if (s) return s;
+    for (int pass = 0; pass < 2; ++pass) {
+        cudaEventRecord(p->ev0, st);
+        s = enqueue_range(p, b, e, p->d_slots, 0, 1, pass == 0 ? -1 : 1);
+        if (s) return s;
+        cudaEventRecord(p->ev1, st);
+        cudaError_t ce = cudaMemcpyAsync(h, p->d_slots, kNSlots * 8, cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+        if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p->ev0, p->ev1);
+        *kms += ms;
+        if (h[SLOT_QFULL] == 0) return BDEG_OK;
+    }
+    return BDEG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void bdeg_default_options(bdeg_options *o) {
+    std::memset(o, 0, sizeof(*o));
+    o->seed = 1;
+    o->lift_bits = 20;
+    o->max_relift = 32;
+    o->device = 0;
+    o->rank = 0;
+    o->world = 1;
+    o->stream = nullptr;
+    o->flags = 0;
+    o->inner_levels = -1;
+    o->ctas_per_sm = 0;
+}
+
+bdeg_status bdeg_plan(const bdeg_problem *prob, const bdeg_options *opt, bdeg_plan_t *out) {
+    if (!prob || !out) return fail(nullptr, BDEG_E_INVALID, "NULL argument");
+    if (prob->n < 1 || prob->m < 0 || (prob->m > 0 && !prob->A))
+        return fail(nullptr, BDEG_E_INVALID, "bad problem shape");
+    const double t0 = now_ms();
+    bdeg_plan_s *p = new bdeg_plan_s();
+    if (opt) p->opt = *opt; else bdeg_default_options(&p->opt);
+    if (p->opt.world < 1) p->opt.world = 1;
+    fill_binom(p->binom);
+    p->n = prob->n;
+    p->m = prob->m;
+    p->A.assign(prob->A, prob->A + (size_t)prob->n * prob->m);
+    if (prob->b_re) p->bre.assign(prob->b_re, prob->b_re + prob->m);
+    if (prob->b_im) p->bim.assign(prob->b_im, prob->b_im + prob->m);
+    p->seed_used = p->opt.seed;
+    if (prob->lifting) {
+        p->user_lift = true;
+        p->lift.assign(prob->lifting, prob->lifting + prob->n + 1);
+    } else {
+        gen_lifting(p->opt.seed, prob->n + 1, p->opt.lift_bits, p->lift);
+    }
+    std::string err;
+    if (!analyze_system(p->n, p->m, p->A.data(), p->bre.empty() ? nullptr : p->bre.data(),
+                        p->bim.empty() ? nullptr : p->bim.data(), !(p->opt.flags & BDEG_FLAG_NO_LLL), p->fe, err)) {
+        delete p;
+        return fail(nullptr, BDEG_E_TOO_LARGE, err);
+    }
+    if (!p->fe.consistent) {
+        delete p;
+        return fail(nullptr, BDEG_E_INCONSISTENT, "inconsistent system: b^{Q_0} != 1 (PAPER.md P:366-367)");
+    }
+    if (p->fe.dim == 0) {
+        p->K = 0;
+        p->N = 0;
+        p->total = 0;
+    } else {
+        rebuild_points(p);
+        bdeg_status s = finish_plan(p);
+        if (s) {
+            g_err = p->err;
+            delete p;
+            return s;
+        }
+    }
+    p->plan_ms = now_ms() - t0;
+    *out = p;
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_plan_points(int32_t K, int32_t N, const int64_t *V, const int64_t *lifting,
+                             const bdeg_options *opt, bdeg_plan_t *out) {
+    if (!V || !out || K < 1 || N < K) return fail(nullptr, BDEG_E_INVALID, "bad point configuration");
+    const double t0 = now_ms();
+    bdeg_plan_s *p = new bdeg_plan_s();
+    if (opt) p->opt = *opt; else bdeg_default_options(&p->opt);
+    if (p->opt.world < 1) p->opt.world = 1;
+    fill_binom(p->binom);
+    p->points_mode = true;
+    p->K = K;
+    p->N = N;
+    p->V.assign(V, V + (size_t)K * N);
+    p->seed_used = p->opt.seed;
+    if (lifting) {
+        p->user_lift = true;
+        p->lift.assign(lifting, lifting + N);
+    } else {
+        gen_lifting(p->opt.seed, N, p->opt.lift_bits, p->lift);
+    }
+    p->w = p->lift;
+    bdeg_status s = finish_plan(p);
+    if (s) {
+        g_err = p->err;
+        delete p;
+        return s;
+    }
+    p->plan_ms = now_ms() - t0;
+    *out = p;
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_plan_info(bdeg_plan_t p, bdeg_result *out) {
+    if (!p || !out) return fail(p, BDEG_E_INVALID, "NULL argument");
+    fill_front(p, out);
+    return BDEG_OK;
+}
+
+size_t bdeg_workspace_bytes(bdeg_plan_t p) { return p && p->K > 0 ? layout(p).total : 0; }
+
+bdeg_status bdeg_set_workspace(bdeg_plan_t p, void *d_ptr, size_t bytes) {
+    if (!p || !d_ptr) return fail(p, BDEG_E_INVALID, "NULL argument");
+    if (p->dev_ready) return fail(p, BDEG_E_INVALID, "workspace already in use");
+    if (bytes < layout(p).total) return fail(p, BDEG_E_INVALID, "workspace too small");
+    if (((uintptr_t)d_ptr & 255) != 0) return fail(p, BDEG_E_INVALID, "workspace must be 256-byte aligned");
+    p->ws = (char *)d_ptr;
+    p->ws_bytes = bytes;
+    p->own_ws = false;
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_relift(bdeg_plan_t p, int32_t attempt) {
+    if (!p) return fail(p, BDEG_E_INVALID, "NULL plan");
+    if (p->user_lift) return fail(p, BDEG_E_INVALID, "the lifting was given by the caller");
+    p->seed_used = derive_seed(p->opt.seed, attempt);
+    const int count = p->points_mode ? p->N : p->n + 1;
+    gen_lifting(p->seed_used, count, p->opt.lift_bits, p->lift);
+    if (p->points_mode) p->w = p->lift;
+    else rebuild_points(p);
+    p->relifts = attempt;
+    p->l_dirty = true;
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_degree(bdeg_plan_t p, bdeg_result *out) {
+    if (!p || !out) return fail(p, BDEG_E_INVALID, "NULL argument");
+    const double t0 = now_ms();
+    bdeg_result r;
+    fill_front(p, &r);
+    if (p->K == 0) {                      // d = 0: isolated points
+        r.deg_lo = 1;
+        r.total_ms = now_ms() - t0;
+        *out = r;
+        return BDEG_OK;
+    }
+    double kms = 0;
+    for (int attempt = p->relifts;; ++attempt) {
+        int64_t h[kNSlots];
+        bdeg_status s = run_sync(p, 0, p->total, h, &kms);
+        if (s) return s;
+        fill_front(p, &r);
+        s = slots_to_result(p, h, &r);
+        if (s) return s;
+        if (r.ties == 0) break;
+        if (p->user_lift || (p->opt.flags & BDEG_FLAG_NO_RELIFT))
+            return fail(p, BDEG_E_DEGENERATE, "degenerate lifting: a would-be cell has a zero facet value");
+        if (attempt + 1 > p->opt.max_relift)
+            return fail(p, BDEG_E_DEGENERATE, "no generic lifting found within max_relift attempts");
+        bdeg_relift(p, attempt + 1);
+    }
+    r.kernel_ms = kms;
+    r.total_ms = now_ms() - t0;
+    *out = r;
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_degree_range(bdeg_plan_t p, uint64_t begin, uint64_t end, bdeg_result *out) {
+    if (!p || !out) return fail(p, BDEG_E_INVALID, "NULL argument");
+    const double t0 = now_ms();
+    bdeg_result r;
+    fill_front(p, &r);
+    if (p->K == 0) {
+        *out = r;
+        return BDEG_OK;
+    }
+    double kms = 0;
+    int64_t h[kNSlots];
+    bdeg_status s = run_sync(p, begin, end, h, &kms);
+    if (s) return s;
+    s = slots_to_result(p, h, &r);
+    if (s) return s;
+    r.kernel_ms = kms;
+    r.total_ms = now_ms() - t0;
+    *out = r;
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_degree_partial(bdeg_plan_t p, int64_t *d_slots) {
+    if (!p || !d_slots) return fail(p, BDEG_E_INVALID, "NULL argument");
+    if (p->K == 0) {
+        cudaError_t ce = cudaMemsetAsync(d_slots, 0, kNSlots * 8, (cudaStream_t)p->opt.stream);
+        return ce == cudaSuccess ? BDEG_OK : fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+    }
+    bdeg_status s = ensure_device(p);
+    if (s) return s;
+    return enqueue_range(p, 0, p->total, reinterpret_cast<unsigned long long *>(d_slots), p->opt.rank,
+                         p->opt.world, -1);
+}
+
+bdeg_status bdeg_finalize(bdeg_plan_t p, const int64_t *h_slots, bdeg_result *out) {
+    if (!p || !h_slots || !out) return fail(p, BDEG_E_INVALID, "NULL argument");
+    bdeg_result r;
+    fill_front(p, &r);
+    if (p->K == 0) {
+        r.deg_lo = 1;
+        *out = r;
+        return BDEG_OK;
+    }
+    if (h_slots[SLOT_QFULL] > 0)
+        return fail(p, BDEG_E_TOO_LARGE, "overflow re-run queue exhausted; rerun with BDEG_FLAG_FORCE_TIER1");
+    bdeg_status s = slots_to_result(p, h_slots, &r);
+    if (s) return s;
+    *out = r;
+    return BDEG_OK;
+}
+
+const char *bdeg_last_error(bdeg_plan_t p) { return p ? p->err.c_str() : g_err.c_str(); }
+
+const char *bdeg_status_str(bdeg_status s) {
+    switch (s) {
+        case BDEG_OK: return "ok";
+        case BDEG_E_INVALID: return "invalid argument";
+        case BDEG_E_INCONSISTENT: return "inconsistent system";
+        case BDEG_E_DEGENERATE: return "degenerate lifting";
+        case BDEG_E_IO: return "io error";
+        case BDEG_E_TOO_LARGE: return "too large";
+        case BDEG_E_CUDA: return "cuda error";
+        case BDEG_E_COMM: return "communication error";
+    }
+    return "unknown";
+}
+
+void bdeg_destroy(bdeg_plan_t p) {
+    if (!p) return;
+    if (p->own_ws && p->ws) cudaFree(p->ws);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    delete p;
+}
+
+uint64_t bdeg_launch_count(void) { return launch_counter_add(0); }
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// Internal declarations shared by the host front end (frontend.cpp,
+// bdeg_capi.cpp) and the CUDA kernels (bdeg_kernels.cu) of libbdeg.so.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace bdeg {
+
+typedef __int128 i128;
+typedef unsigned __int128 u128;
+
+constexpr int kMaxN = 64;    // points: the kernel maps one point to a lane slot (2 slots/lane)
+constexpr int kMaxK = 32;    // subset size (K+1 rows of the lifted matrix, <= 33)
+constexpr int kBinomRows = 65;
+constexpr int kBinomCols = 34;
+
+// ----------------------------------------------------------------- front end
+struct FrontEnd {
+    int n = 0, m = 0, rank = 0, dim = 0;
+    u128 components = 1;
+    bool consistent = true;
+    bool homogeneous = false;
+    std::vector<std::vector<i128>> P0;   // dim x n (rows = basis of the left kernel lattice)
+};
+
+// SNF-based analysis of x^A = b.  Returns false with
+// `err` set on arithmetic overflow.
+bool analyze_system(int n, int m, const int64_t *A, const double *b_re, const double *b_im,
+                    bool lll, FrontEnd &fe, std::string &err);
+
+// Point configuration (Prop. 4; readings Z2/Z5): distinct non-zero
+// columns of P0 in first-occurrence order (min lifting on merge), then the
+// origin (generic case, K = d+1, v = (1, a)), or only the columns (homogeneous
+// pyramid case, K = d).  lifting: n+1 values.  V is point-major N x K.
+void build_points(const FrontEnd &fe, const int64_t *lifting, bool homog_shortcut,
+                  int &K, int &N, std::vector<int64_t> &V, std::vector<int64_t> &w,
+                  std::vector<int> &point_of_var, int &origin_index);
+
+// SplitMix64 (DESIGN.md input recipe; the same generator workloads/ uses).
+struct SplitMix64 {
+    uint64_t s;
+    explicit SplitMix64(uint64_t seed) : s(seed) {}
+    uint64_t next() {
+        s += 0x9E3779B97F4A7C15ull;
+        uint64_t z = s;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }
+};
+uint64_t derive_seed(uint64_t seed, int attempt);
+
+// ----------------------------------------------------------------- kernels
+struct DeviceProblem {
+    const int64_t *L;        // (K+1) x N lifted matrix, column-major: L[l*(K+1) + i]
+    const uint64_t *binom;   // kBinomRows x kBinomCols
+    int K, N, S, T;          // subset size, points, inner levels, top (block) levels
+};
+
+struct LaunchArgs {
+    DeviceProblem P;
+    uint64_t rank_begin, rank_end;    // candidate colex ranks [begin, end)
+    uint64_t blk_first, blk_last;     // inclusive block-id range covering [begin, end)
+    uint64_t blk_offset, blk_stride;  // this GPU takes blocks blk_last - (offset + i*stride)
+    unsigned long long *counter;      // work-stealing counter (zeroed before launch)
+    unsigned long long *slots;        // kNSlots accumulators
+    unsigned long long *ovf_queue;    // block ids whose int32-tier run overflowed
+    unsigned long long *ovf_count;
+    uint64_t ovf_cap;
+    int tier;                         // 0: int32 values / int64 products, 1: int64 / int128
+    int replay;                       // 1: process ovf_queue[0..*ovf_count) in tier 1
+    int grid, block;                  // launch shape
+    void *stream;
+};
+
+constexpr int kNSlots = 16;
+enum Slot {
+    SLOT_VOL0 = 0, SLOT_VOL1, SLOT_VOL2, SLOT_VOL3,   // 32-bit limbs of the volume
+    SLOT_CELLS = 4, SLOT_SINGULAR = 5, SLOT_CAND = 6, SLOT_TIES = 7,
+    SLOT_OVF_BLOCKS = 8,   // int32-tier blocks queued for re-run
+    SLOT_FATAL = 9,        // int64-tier overflow (value beyond int64)
+    SLOT_QFULL = 10,       // overflow queue exhausted
+    SLOT_BLOCKS = 11, SLOT_UPDATES = 12, SLOT_LEAVES = 13
+};
+
+// Dynamic shared memory bytes for a launch of the enumeration kernel.
+size_t enumerate_smem_bytes(int K, int N, int warps_per_cta);
+// Launch k_enumerate (returns cudaError_t as int).
+int launch_enumerate(const LaunchArgs &a);
+int kernel_warps_per_cta();
+// Max resident CTAs per SM for this configuration (occupancy API).
+int enumerate_max_ctas_per_sm(const LaunchArgs &a);
+
+uint64_t launch_counter_add(uint64_t k);
+
+}  // namespace bdeg

@@ -1,0 +1,240 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+element by element (degree, cells, singular, candidates, ties) on the same
+seeded inputs.  All of this is integer work, so the bar is bit-exact.
+"""
+import math
+import random
+
+import pytest
+
+import workloads as W
+from oracle import enumerate_lifted, point_configuration
+from oracle.native import enumerate_range
+
+B = pytest.importorskip("paper_1501_02237_b200")
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("volume", "cells", "singular", "candidates", "ties")
+
+
+def _gpu(r):
+    return {"volume": r.degree, "cells": r.cells, "singular": r.singular,
+            "candidates": r.candidates, "ties": r.ties}
+
+
+def _oracle_system(A, b, lift, threads=8):
+    cfg = point_configuration(A, b, lift)
+    K, V, w = cfg["cone"]
+    return enumerate_range(K, V, w, threads=threads), cfg
+
+
+def _assert_same(g, o, what=""):
+    for k in KEYS:
+        assert g[k] == o[k], (what, k, g, o)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+SYSTEMS = ["twisted_cubic", "conifold", "dp0", "W1_2", "W1_3", "W1_4", "W1_5", "W1_6",
+           "W2_1", "W3_1", "W2_2", "W2_3", "rnc3", "rnc7", "rnc20"]
+
+
+@pytest.mark.parametrize("name", SYSTEMS)
+def test_systems_full(name):
+    A, b = W.named_system(name)
+    lift = W.liftings(len(A) + 1, 1)
+    o, cfg = _oracle_system(A, b, lift)
+    r = B.Plan.from_system(A, b, lift).degree()
+    assert r.K == cfg["cone"][0] and r.N == len(cfg["cone"][1])
+    assert r.dim == cfg["dim"] and r.components == cfg["components"]
+    _assert_same(_gpu(r), o, name)
+
+
+@pytest.mark.parametrize("seed", [5, 31, 46, 66])
+@pytest.mark.parametrize("flags", [0, 0x1])          # LLL basis and raw SNF basis
+def test_c2_random_systems(seed, flags):
+    A, b, lift = W.c2_system(seed)
+    o, cfg = _oracle_system(A, b, lift)
+    r = B.Plan.from_system(A, b, lift, flags=flags).degree()
+    assert r.components == cfg["components"] > 1
+    _assert_same(_gpu(r), o, seed)
+
+
+def test_toric_closed_forms():
+    for sysf, want in [(W.segre_system(2, 3), 10), (W.veronese_system(2, 3), 8),
+                       (W.veronese_system(3, 2), 9), (W.segre_system(1, 4), 5)]:
+        A, b = sysf
+        lift = W.liftings(len(A) + 1, 2)
+        o, _ = _oracle_system(A, b, lift)
+        r = B.Plan.from_system(A, b, lift).degree()
+        _assert_same(_gpu(r), o)
+        assert r.degree == want
+
+
+@pytest.mark.parametrize("inner", [0, 1, 2, 3])
+@pytest.mark.parametrize("tierflag", [0x4, 0x8])
+def test_inner_levels_and_tiers(inner, tierflag):
+    # every register-DFS depth and both arithmetic tiers give identical counts
+    for (n_pts, dim, seed) in [(14, 4, 1), (33, 3, 2), (40, 4, 3), (64, 2, 4)]:
+        V, w = W.c5_points(seed, n_points=n_pts, dim=dim)
+        K = dim + 1
+        o = enumerate_range(K, V, w, threads=8)
+        r = B.Plan.from_points(V, w, inner_levels=inner, flags=tierflag).degree()
+        _assert_same(_gpu(r), o, (n_pts, dim, inner, tierflag))
+
+
+def test_tier0_overflow_rerun():
+    # raw SNF basis of C2 needs > 31-bit values: the int32 tier must hand the
+    # affected blocks to the int64 tier and still be exact
+    A, b, lift = W.c2_system(5)
+    o, _ = _oracle_system(A, b, lift)
+    r = B.Plan.from_system(A, b, lift, flags=0x1 | 0x4, inner_levels=0).degree()
+    assert r.overflow_reruns > 0
+    _assert_same(_gpu(r), o)
+
+
+def test_random_point_sets():
+    # SPEC S:477 style: many small random configurations, d <= 4
+    rng = random.Random(5)
+    done = 0
+    for seed in range(300):
+        d = 1 + seed % 4
+        pts, _ = W.random_point_set(seed, d, d + 2 + seed % 9, -2, 2)
+        pts = list(dict.fromkeys(pts))
+        if len(pts) < d + 1:
+            continue
+        V = [(1,) + p for p in pts]
+        w = W.liftings(len(V), 500 + seed)
+        o = enumerate_lifted(d + 1, V, w)
+        if o["volume"] == 0:
+            continue
+        r = B.Plan.from_points(V, w, inner_levels=rng.randint(0, 3)).degree_range(0, math.comb(len(V), d + 1))
+        _assert_same(_gpu(r), o, seed)
+        done += 1
+    assert done > 100
+
+
+def test_rank_ranges_c5_full_size():
+    # C5: K = 8 over 40 points, 7.7e7 candidates; sampled rank
+    # intervals against the oracle, in the launch configuration bench.py uses
+    V, w = W.c5_points(1)
+    plan = B.Plan.from_points(V, w)
+    total = math.comb(40, 8)
+    rng = random.Random(11)
+    for _ in range(12):
+        b = rng.randrange(0, total - 30000)
+        e = b + rng.randrange(1, 30000)
+        o = enumerate_range(8, V, w, b, e, threads=8)
+        r = plan.degree_range(b, e)
+        _assert_same(_gpu(r), o, (b, e))
+    # the first and last ranks and a tiny interval
+    for (b, e) in [(0, 5000), (total - 4000, total), (123456, 123457)]:
+        _assert_same(_gpu(plan.degree_range(b, e)), enumerate_range(8, V, w, b, e, threads=8), (b, e))
+
+
+@pytest.mark.parametrize("mk", [(2, 4), (3, 3), (2, 5)])
+def test_master_space_ranges(mk):
+    A, b = W.master_space_system(*mk)
+    lift = W.liftings(len(A) + 1, 1)
+    cfg = point_configuration(A, b, lift)
+    K, V, w = cfg["cone"]
+    plan = B.Plan.from_system(A, b, lift)
+    total = math.comb(len(V), K)
+    rng = random.Random(mk[0] * 10 + mk[1])
+    for _ in range(6):
+        b0 = rng.randrange(0, total - 20000)
+        e0 = b0 + rng.randrange(1, 20000)
+        _assert_same(_gpu(plan.degree_range(b0, e0)), enumerate_range(K, V, w, b0, e0, threads=8), (b0, e0))
+
+
+def test_table3_degrees_gpu(table3):
+    # Table 3 exact entries within brute-force reach on one B200
+    for mk in [(1, 7), (1, 8), (2, 4), (3, 3), (2, 5), (5, 1), (8, 1)]:
+        A, b = W.master_space_system(*mk)
+        r = B.degree(A, b, seed=1)
+        assert r.degree == table3[mk][0], mk
+        assert r.components == 1 and r.ties == 0
+        assert r.candidates == r.total_candidates == math.comb(r.N, r.K)
+
+
+def test_lifting_invariance_gpu():
+    A, b = W.master_space_system(2, 4)
+    degs = {B.degree(A, b, seed=s).degree for s in (1, 2, 3)}
+    assert degs == {584}
+    sing = {B.degree(A, b, seed=s).singular for s in (1, 2, 3)}
+    assert len(sing) == 1
+
+
+def test_degenerate_user_lifting_raises():
+    V, _ = W.c5_points(4, n_points=10, dim=3)
+    with pytest.raises(B.BdegError) as ei:
+        B.degree_points(V, [7] * 10)
+    assert ei.value.status == 3
+    # the same through a range call reports the ties instead
+    r = B.Plan.from_points(V, [7] * 10).degree_range(0, math.comb(10, 4))
+    assert r.ties == enumerate_lifted(4, V, [7] * 10)["ties"] > 0
+
+
+def test_generated_lifting_relifts():
+    # 1-bit generated liftings are degenerate; the library re-lifts with
+    # derived seeds until the subdivision is regular
+    A, b = W.master_space_system(2, 2)
+    r = B.degree(A, b, seed=3, lift_bits=2)
+    assert r.degree == 14
+    assert r.relifts >= 0 and r.ties == 0
+
+
+def test_errors_and_degenerate_dimensions():
+    with pytest.raises(B.BdegError) as ei:
+        B.degree([[1, 1], [0, 0]], [1, 2])
+    assert ei.value.status == 2
+    r = B.degree([[2, 0], [0, 3]])
+    assert r.dim == 0 and r.degree == 1 and r.components == 6
+    # K = 1 and K = N edge cases
+    V = [(3,), (1,), (2,), (5,)]
+    w = [4, 9, 1, 7]
+    _assert_same(_gpu(B.degree_points(V, w)), enumerate_lifted(1, V, w))
+    V, w = W.c5_points(9, n_points=6, dim=5)
+    _assert_same(_gpu(B.degree_points(V, w)), enumerate_lifted(6, V, w))
+
+
+def test_torch_workspace_and_stream():
+    A, b = W.master_space_system(2, 3)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        plan = B.Plan.from_system(A, b, seed=1)
+        ws = plan.use_torch_workspace()
+        assert ws is not None and ws.is_cuda
+        r = plan.degree()
+    assert r.degree == 92
+
+
+def test_partial_shards_sum_to_full():
+    # what each rank of a world-4 job computes, summed on one GPU
+    V, w = W.c5_points(2, n_points=36, dim=5)
+    full = B.Plan.from_points(V, w).degree()
+    tot = [0] * B.NSLOTS
+    for rank in range(4):
+        plan = B.Plan.from_points(V, w, rank=rank, world=4)
+        slots = torch.zeros(B.NSLOTS, dtype=torch.int64, device="cuda")
+        plan.degree_partial(slots.data_ptr())
+        torch.cuda.synchronize()
+        for i, v in enumerate(slots.cpu().tolist()):
+            tot[i] += v
+    r = B.Plan.from_points(V, w).finalize(tot)
+    assert (r.degree, r.cells, r.singular, r.candidates) == (full.degree, full.cells, full.singular, full.candidates)
+
+
+@pytest.mark.slow
+def test_w34_w26_full():
+    # 3.8e9 candidates each (Table 3: 26762 and 22304)
+    for mk, want in [((3, 4), 26762), ((2, 6), 22304)]:
+        A, b = W.master_space_system(*mk)
+        assert B.degree(A, b, seed=1).degree == want
