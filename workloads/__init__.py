@@ -239,6 +239,8 @@ def c5_points(seed: int, n_points: int = 40, dim: int = 7, lo: int = -3, hi: int
     """n_points distinct a in [lo,hi]^dim, V_l = (1, a_l)
     in generation order, then n_points liftings.  Returns (V point-major
     list of (dim+1)-tuples, lifting list)."""
+    if n_points > (hi - lo + 1) ** dim:
+        raise ValueError("not enough distinct lattice points in the box")
     rng = SplitMix64(seed)
     seen, pts = set(), []
     while len(pts) < n_points:
