@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""Benchmark: exact degree (normalised lattice volume) of the C5 synthetic
+configuration — BASELINE.json configs[4], "k=8 over 40 lifted lattice points
+(~7.7e7 candidate simplices), rank space sharded across 8xB200".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|w26|w34|w27|w24]
+  python bench.py --impl reference ...        # the CPU oracle arm
+
+A step = one pass of the whole hot path over the full rank space: the
+enumeration kernel (+ int64-tier replay), the exact combine (one NCCL
+all-reduce of 16 int64 slots when N > 1) and the D2H read of the slots.
+`value` (simplices/s) = C(N,K) / device time per step, max over ranks,
+inputs resident in HBM.  `e2e` = the same metric through the C ABI with
+HOST buffers (bdeg_plan_points + bdeg_degree: H2D upload of the lifted
+matrix and binomial table, D2H of the result) per step.
+
+Timing rules: W untimed warm-up steps; each timed step bracketed by CUDA
+events on the launching stream; L2 flushed between steps (256 MiB write,
+outside the events); barrier + synchronize around the timed region; the
+clocks are sampled with nvidia-smi during it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import random
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simplices/sec and time-to-degree at 1/2/4/8 B200; % integer-pipe peak"
+UNIT = "simplices/s"
+
+
+def workload(name):
+    """-> (description, K, V point-major, lifting, extra config dict)."""
+    import workloads as W
+    if name == "c5":
+        V, w = W.c5_points(1)
+        return ("C5 synthetic: K=8 vectors (1,a), a uniform in [-3,3]^7, N=40 distinct points, "
+                "lifting uniform in [0,2^20) (SplitMix64 seed 1)", 8, V, w, {"seed": 1})
+    m, k = {"w24": (2, 4), "w33": (3, 3), "w25": (2, 5), "w26": (2, 6), "w34": (3, 4),
+            "w27": (2, 7)}[name]
+    from oracle import point_configuration  # input preparation only (front end of the oracle)
+    A, b = W.master_space_system(m, k)
+    lift = W.liftings(len(A) + 1, 1)
+    cfg = point_configuration(A, b, lift)
+    K, V, w = cfg["cone"]
+    return (f"master space grad W_{{{m},{k}}} (PAPER.md Table 3), lifted point configuration "
+            f"K={K}, N={len(V)}", K, V, w, {"m": m, "k": k, "seed": 1})
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bdeg_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        try:
+            rows = [l.strip().split(", ") for l in open(self.path) if l.strip()]
+        except Exception:  # noqa: BLE001
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 4 + i and "Active" in r[4 + i]
+                          and "Not" not in r[4 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(rows), "reasons": reasons}
+
+
+def cpu_oracle_sample(K, V, w, budget_candidates, seed=7):
+    """Time the CPU oracle (C variant, all host cores) on random rank intervals."""
+    from oracle.native import enumerate_range
+    total = math.comb(len(V), K)
+    rng = random.Random(seed)
+    n_iv = 16
+    span = max(1, min(total, budget_candidates) // n_iv)
+    ivs = []
+    for _ in range(n_iv):
+        b = rng.randrange(0, max(1, total - span))
+        ivs.append((b, min(total, b + span)))
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    cand = 0
+    for b, e in ivs:
+        r = enumerate_range(K, V, w, b, e, threads=cores)
+        cand += r["candidates"]
+    dt = time.perf_counter() - t0
+    return cand / dt, cores, f"{n_iv} random colex-rank intervals of {span} candidates ({cand} total) of the same workload"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    desc, K, V, w, extra = workload(args.workload)
+    total = math.comb(len(V), K)
+    budget = args.ref_sample
+    for _ in range(args.warmup):
+        cpu_oracle_sample(K, V, w, budget // 4, seed=1)
+    vals = []
+    t0 = time.perf_counter()
+    sample = None
+    for s in range(args.steps):
+        v, cores, sample = cpu_oracle_sample(K, V, w, budget, seed=100 + s)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * wall / max(1, args.steps),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int128",
+        "data": "synthetic",
+        "config": {"workload": desc, "K": K, "N": len(V), "candidates": total, **extra},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "time_to_degree_s_extrapolated": total / value,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1501_02237_b200 as B
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    desc, K, V, w, extra = workload(args.workload)
+    total = math.comb(len(V), K)
+    stream = torch.cuda.current_stream()
+
+    plan = B.Plan.from_points(V, w, rank=rank, world=world, stream=stream.cuda_stream)
+    plan.use_torch_workspace(local)
+    info = plan.info()
+    slots = torch.zeros(B.NSLOTS, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        plan.degree_partial(slots.data_ptr())
+        if world > 1:
+            dist.all_reduce(slots, op=dist.ReduceOp.SUM)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    res = plan.finalize(slots.cpu().tolist())
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = B.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for s in range(args.steps):
+            flush.fill_(float(s))                       # L2 flush (outside the events)
+            evs[s][0].record(stream)
+            step()
+            evs[s][1].record(stream)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+        if world > 1:
+            dist.barrier()
+    launches = B.launch_count() - launches0
+    ms = [a.elapsed_time(b) for a, b in evs]
+    ms_step = statistics.mean(ms)
+    tt = torch.tensor([ms_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_step = float(tt.item())
+    res = plan.finalize(slots.cpu().tolist())
+    value = total / (ms_step / 1000.0)
+
+    # ---- e2e: the public C-ABI call with HOST buffers, every step
+    e2e_ms = []
+    h2d = (((K + 1) * len(V) * 8 + 15) // 16) * 16 + 65 * 34 * 8
+    d2h = B.NSLOTS * 8
+    for s in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        with B.Plan.from_points(V, w, rank=rank, world=world, stream=stream.cuda_stream) as p2:
+            if world == 1:
+                r2 = p2.degree()
+            else:
+                sl = torch.zeros(B.NSLOTS, dtype=torch.int64, device=dev)
+                p2.degree_partial(sl.data_ptr())
+                dist.all_reduce(sl, op=dist.ReduceOp.SUM)
+                r2 = p2.finalize(sl.cpu().tolist())
+        dt = (time.perf_counter() - t0) * 1000.0
+        if s >= args.warmup:
+            e2e_ms.append(dt)
+        assert r2.degree == res.degree
+    e2e = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    e2e_step = float(e2e.item())
+
+    if rank == 0:
+        peaks, peak_kind = load_peaks()
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_ops = 128.0 * n_sm * sm_mhz * 1e6 * world         # 4 SMSP x 32 lanes issue / clk / SM
+        # algorithmic integer ops per step: 4 per
+        # fraction-free update (2 mul, 1 sub, 1 exact division) + 2 per
+        # point per leaf facet test (slope key, compare)
+        alg_ops = 4.0 * res.updates + 2.0 * res.leaves * len(V)
+        achieved = alg_ops / (ms_step / 1000.0)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(args.workload)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, sample = cpu_oracle_sample(K, V, w, args.ref_sample)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": B.bdeg.TIER_DTYPE[info.tier],
+            "data": "synthetic",
+            "config": {"workload": desc, "K": K, "N": len(V), "candidates": total,
+                       "l2": "flushed between steps (256 MiB write outside the timed events)",
+                       "inner_levels": info.inner_levels, "tier": info.tier,
+                       "parallelism": f"rank-space blocks interleaved over {world} GPU(s)", **extra},
+            "time_to_degree_ms": e2e_step,
+            "result": {"degree": res.degree, "cells": res.cells, "singular": res.singular,
+                       "candidates": res.candidates, "ties": res.ties,
+                       "overflow_reruns": res.overflow_reruns},
+            "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
+                         "unit": "Tintop/s", "frac": achieved / peak_ops, "traffic": traffic,
+                         "peak_basis": f"128 int lane-ops/clk/SM x {n_sm} SMs x {sm_mhz:.0f} MHz "
+                                       f"({peak_kind} sm_max_mhz) x {world} GPU(s)",
+                         "algorithmic_ops_per_step": alg_ops},
+            "cpu_baseline": cpu,
+            "e2e": {"value": total / (e2e_step / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "wall_s_timed_region": t_wall,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="bdeg", choices=["bdeg", "reference"])
+    ap.add_argument("--workload", default="c5")
+    ap.add_argument("--ref-sample", type=int, default=4_000_000,
+                    help="candidates per oracle sample (cpu_baseline / reference arm)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

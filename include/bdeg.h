@@ -45,7 +45,7 @@ typedef enum {
     BDEG_E_DEGENERATE = 3,    /* lifting not generic ("almost all"); user-given
                                  lifting, or max_relift generated liftings exhausted  */
     BDEG_E_IO = 4,            /* reserved (SPEC exit code 4)                           */
-    BDEG_E_TOO_LARGE = 5,     /* N > 64, K > 32, or an exact value exceeds int64       */
+    BDEG_E_TOO_LARGE = 5,     /* N > 64, K > 32, or an exact value exceeds 2^62        */
     BDEG_E_CUDA = 6,          /* CUDA runtime error / no sm_100 device                 */
     BDEG_E_COMM = 7           /* reserved for the multi-GPU combine                    */
 } bdeg_status;
@@ -65,8 +65,9 @@ typedef struct {
 /* options.flags */
 #define BDEG_FLAG_NO_LLL            0x1u  /* keep the SNF basis of P_0 (no LLL reduction)     */
 #define BDEG_FLAG_NO_HOMOG_SHORTCUT 0x2u  /* always K = d+1 with the origin (no pyramid K = d)  */
-#define BDEG_FLAG_FORCE_TIER0       0x4u  /* start in the int32 tier even if the planner would not */
-#define BDEG_FLAG_FORCE_TIER1       0x8u  /* skip the int32 tier                                  */
+#define BDEG_FLAG_FORCE_TIER0       0x4u  /* start in tier 0: int32 values, int64 products            */
+#define BDEG_FLAG_FORCE_TIER1       0x8u  /* start in tier 1: int32 V rows / int64 lift row, int64 products */
+#define BDEG_FLAG_FORCE_TIER2       0x20u /* tier 2 only: int64 values, checked int128 products       */
 #define BDEG_FLAG_NO_RELIFT         0x10u /* report BDEG_E_DEGENERATE instead of re-lifting       */
 
 typedef struct {
@@ -77,7 +78,7 @@ typedef struct {
     int32_t rank, world;     /* this process's shard of rank space (default 0, 1)    */
     void *stream;            /* cudaStream_t for every launch/copy; NULL = default   */
     uint32_t flags;          /* BDEG_FLAG_*                                          */
-    int32_t inner_levels;    /* register-resident DFS depth S in 0..3; -1 = auto     */
+    int32_t inner_levels;    /* register-resident DFS depth S in 0..6; -1 = auto     */
     int32_t ctas_per_sm;     /* persistent CTAs per SM; 0 = auto                     */
 } bdeg_options;
 
@@ -85,7 +86,7 @@ typedef struct {
     /* front end (bdeg_plan / bdeg_plan_info) */
     int32_t n, rank, dim;    /* dim = n - rank (Prop. 1)                             */
     int32_t K, N;            /* subset size and number of lifted points              */
-    int32_t tier;            /* arithmetic tier the enumeration started in (0 or 1)  */
+    int32_t tier;            /* arithmetic tier the enumeration started in (0, 1, 2) */
     int32_t homogeneous;     /* 1 if 1^T A = 0 (K = d, pyramid reading)              */
     int32_t inner_levels;    /* S used by the kernel                                 */
     uint64_t comp_lo, comp_hi;        /* |prod d_j| as unsigned 128-bit      */
@@ -95,7 +96,7 @@ typedef struct {
     uint64_t cells;          /* cells of the regular subdivision (lifting-dependent) */
     uint64_t singular;       /* K-subsets with det = 0 (lifting-independent)         */
     uint64_t ties;           /* would-be cells with a zero facet value (degenerate)  */
-    uint64_t overflow_reruns;/* blocks re-run in the int64 tier                      */
+    uint64_t overflow_reruns;/* blocks re-run in tier 2 after leaving their tier     */
     uint64_t updates;        /* fraction-free elimination updates executed          */
     uint64_t leaves;         /* (K-1)-prefixes tested (each = one warp-wide facet test) */
     int32_t relifts;         /* re-lift attempts used                                */

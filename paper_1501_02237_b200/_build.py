@@ -21,15 +21,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_lib(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build_lib(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    if out == LIB and not force and not _stale():
         return LIB
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"),
-           "-o", LIB + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES] + ["-lcudart"]
+           *[f"-D{d}" for d in defines], "-o", out + ".tmp"] + \
+        [os.path.join(CSRC, f) for f in SOURCES] + ["-lcudart"]
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

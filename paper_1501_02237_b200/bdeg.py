@@ -16,7 +16,7 @@ import os
 from dataclasses import dataclass, field
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbdeg.so")
+LIB_PATH = os.environ.get("BDEG_LIB") or os.path.join(_HERE, "libbdeg.so")  # BDEG_LIB: tuning builds
 
 BDEG_OK = 0
 BDEG_E_INVALID = 1
@@ -32,6 +32,8 @@ FLAG_NO_HOMOG_SHORTCUT = 0x2
 FLAG_FORCE_TIER0 = 0x4
 FLAG_FORCE_TIER1 = 0x8
 FLAG_NO_RELIFT = 0x10
+FLAG_FORCE_TIER2 = 0x20
+TIER_DTYPE = {0: "int32", 1: "int32/int64", 2: "int64/int128"}
 
 NSLOTS = 16
 

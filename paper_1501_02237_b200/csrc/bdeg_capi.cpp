@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -27,7 +28,8 @@ struct bdeg_plan_s {
     int K = 0, N = 0, origin_index = -1;
     std::vector<int64_t> V, w;        // point-major N x K, and N lifts
     std::vector<int> point_of_var;
-    int tier = 0, S = 0, T = 0;
+    int tier = 0, S = 0, T = 0, D = 0;
+    int bits_v = 30, bits_l = 31;
     uint64_t nblocks = 0, total = 0;
     uint64_t seed_used = 0;
     int relifts = 0;
@@ -111,23 +113,27 @@ void unrank(const std::vector<uint64_t> &B, uint64_t r, int K, std::vector<int> 
     }
 }
 
+// work item (D-tuple of the largest indices, colex id) containing `rank`
 uint64_t block_of(const bdeg_plan_s *p, uint64_t rank) {
-    if (p->T == 0) return 0;
+    if (p->D == 0) return 0;
     std::vector<int> c;
     unrank(p->binom, rank, p->K, c);
+    const int kd = p->K - p->D;
     uint64_t b = 0;
-    for (int t = 0; t < p->T; ++t) b += C(p->binom, c[p->S + 1 + t] - p->S - 1, t + 1);
+    for (int t = 0; t < p->D; ++t) b += C(p->binom, c[kd + t] - kd, t + 1);
     return b;
 }
 
-// Largest magnitude (bits) of the fraction-free elimination values along a
-// few sampled prefixes — steers the choice of the starting tier only (the
-// kernel checks every value anyway).
-int sample_bits(const bdeg_plan_s *p) {
+// Largest magnitudes (bits) of the fraction-free elimination values of the
+// V rows and of the lift row along sampled prefixes, as the kernel computes
+// them — steers the choice of the starting tier only (the kernel checks every
+// stored value against its tier's bounds and re-runs offending blocks).
+void sample_bits(const bdeg_plan_s *p, int &bv, int &bl) {
     const int K = p->K, N = p->N;
     SplitMix64 g(0x5eed ^ p->seed_used);
-    i128 mx = 1;
-    for (int s = 0; s < 96; ++s) {
+    i128 mv = 1, ml = 1;
+    bool big = false;
+    for (int s = 0; s < 128 && !big; ++s) {
         std::vector<int> perm(N);
         for (int i = 0; i < N; ++i) perm[i] = i;
         for (int i = N - 1; i > 0; --i) std::swap(perm[i], perm[g.next() % (uint64_t)(i + 1)]);
@@ -138,13 +144,12 @@ int sample_bits(const bdeg_plan_s *p) {
         }
         std::vector<char> alive(K, 1);
         i128 prev = 1;
-        for (int t = 0; t < K - 1; ++t) {
+        for (int t = 0; t < K - 1 && !big; ++t) {
             const int piv_c = perm[t];
             int r = -1;
             for (int i = 0; i < K; ++i) if (alive[i] && M[i][piv_c] != 0) { r = i; break; }
             if (r < 0) break;
             const i128 piv = M[r][piv_c];
-            bool big = false;
             for (int i = 0; i <= K && !big; ++i) {
                 if (i == r || (i < K && !alive[i])) continue;
                 const i128 ci = M[i][piv_c];
@@ -152,45 +157,56 @@ int sample_bits(const bdeg_plan_s *p) {
                     i128 a, b2;
                     if (__builtin_mul_overflow(piv, M[i][l], &a) || __builtin_mul_overflow(ci, M[r][l], &b2)) { big = true; break; }
                     M[i][l] = (a - b2) / prev;
-                    i128 v = M[i][l] < 0 ? -M[i][l] : M[i][l];
-                    if (v > mx) mx = v;
+                    const i128 v = M[i][l] < 0 ? -M[i][l] : M[i][l];
+                    if (i < K) { if (v > mv) mv = v; } else { if (v > ml) ml = v; }
                 }
             }
-            if (big) return 127;
             alive[r] = 0;
             prev = piv;
         }
     }
-    int bits = 0;
-    while (mx > 0) { ++bits; mx >>= 1; }
-    return bits;
+    auto nbits = [](i128 x) { int b = 0; while (x > 0) { ++b; x >>= 1; } return b; };
+    bv = big ? 127 : nbits(mv);
+    bl = big ? 127 : nbits(ml);
+    for (int l = 0; l < N; ++l) {      // the level-0 values themselves
+        int64_t a = p->w[l] < 0 ? -p->w[l] : p->w[l];
+        bl = std::max(bl, nbits((i128)a));
+        for (int i = 0; i < K; ++i) {
+            int64_t v = p->V[(size_t)l * K + i];
+            bv = std::max(bv, nbits((i128)(v < 0 ? -v : v)));
+        }
+    }
 }
 
 void choose_tier_and_blocks(bdeg_plan_s *p) {
     p->total = C(p->binom, p->N, p->K);
-    const int bits = sample_bits(p);
-    p->tier = (bits <= 26) ? 0 : 1;
+    int bv = 0, bl = 0;
+    sample_bits(p, bv, bl);
+    p->bits_v = std::min(30, std::max(bv + 2, 8));
+    p->bits_l = 61 - p->bits_v;
+    if (bv <= 28 && bl <= 28) p->tier = 0;
+    else if (bv + 2 <= 30 && bl < p->bits_l) p->tier = 1;
+    else p->tier = 2;
     if (p->opt.flags & BDEG_FLAG_FORCE_TIER0) p->tier = 0;
     if (p->opt.flags & BDEG_FLAG_FORCE_TIER1) p->tier = 1;
-    const int smax = std::min(3, p->K - 1);
-    int S = -1;
-    if (p->opt.inner_levels >= 0) {
-        S = std::min(p->opt.inner_levels, smax);
-    } else {
-        const uint64_t target = 1u << 16;
-        for (int s = smax; s >= 0; --s)
-            if (C(p->binom, p->N - s - 1, p->K - 1 - s) >= target) { S = s; break; }
-        if (S < 0) {   // small problem: maximise the number of blocks
-            uint64_t best = 0;
-            for (int s = 0; s <= smax; ++s) {
-                const uint64_t nb = C(p->binom, p->N - s - 1, p->K - 1 - s);
-                if (nb > best) { best = nb; S = s; }
-            }
-        }
-    }
-    p->S = std::max(S, 0);
+    if (p->opt.flags & BDEG_FLAG_FORCE_TIER2) p->tier = 2;
+    // Register-DFS depth S (deep: the DFS does one fraction-free step per
+    // tree node), smem prefix T = K-1-S, and the work-item depth D >= T chosen
+    // so that the largest item C(N-D, K-D) is a small fraction of the
+    // per-warp share (items are processed largest-first).
+    const int smax = std::min(kMaxInner, p->K - 1);
+    // measured (tools/sweep_libs.sh): S = 3 for K = 8, 4-5 for K = 12, 6 for K >= 14
+    const int sauto = std::min(smax, std::max(3, p->K / 2 - 1));
+    p->S = p->opt.inner_levels >= 0 ? std::min(p->opt.inner_levels, smax) : sauto;
     p->T = p->K - 1 - p->S;
-    p->nblocks = C(p->binom, p->N - p->S - 1, p->T);
+    const double warps = 148.0 * 16.0;
+    double factor = 0.25;
+    if (const char *e = std::getenv("BDEG_ITEM_FACTOR")) factor = std::atof(e);   // tuning knob
+    const double limit = std::max(1.0, (double)p->total / (warps * factor));
+    int D = p->T;
+    while (D < p->K - 1 && (double)C(p->binom, p->N - D, p->K - D) > limit) ++D;
+    p->D = D;
+    p->nblocks = C(p->binom, p->N - p->K + p->D, p->D);
 }
 
 bdeg_status finish_plan(bdeg_plan_s *p) {
@@ -282,7 +298,7 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     LaunchArgs a{};
     a.P.L = p->d_L;
     a.P.binom = p->d_B;
-    a.P.K = p->K; a.P.N = p->N; a.P.S = p->S; a.P.T = p->T;
+    a.P.K = p->K; a.P.N = p->N; a.P.S = p->S; a.P.T = p->T; a.P.D = p->D;
     a.rank_begin = b;
     a.rank_end = e;
     a.blk_first = block_of(p, b);
@@ -296,12 +312,14 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     a.grid = p->grid;
     a.stream = st;
     a.tier = force_tier >= 0 ? force_tier : p->tier;
+    a.bits_v = p->bits_v;
+    a.bits_l = p->bits_l;
     a.replay = 0;
     a.counter = p->d_ctr + 0;
     int rc = launch_enumerate(a);
     if (rc) return fail(p, BDEG_E_CUDA, std::string("k_enumerate launch: ") + cudaGetErrorString((cudaError_t)rc));
-    if (a.tier == 0) {   // re-run the blocks that left the int32 tier, in int64
-        a.tier = 1;
+    if (a.tier != 2) {   // re-run the blocks that left their tier, in int64/int128
+        a.tier = 2;
         a.replay = 1;
         a.counter = p->d_ctr + 1;
         rc = launch_enumerate(a);
@@ -354,7 +372,7 @@ bdeg_status run_sync(bdeg_plan_s *p, uint64_t b, uint64_t e, int64_t *h, double 
     if (s) return s;
     for (int pass = 0; pass < 2; ++pass) {
         cudaEventRecord(p->ev0, st);
-        s = enqueue_range(p, b, e, p->d_slots, 0, 1, pass == 0 ? -1 : 1);
+        s = enqueue_range(p, b, e, p->d_slots, 0, 1, pass == 0 ? -1 : 2);
         if (s) return s;
         cudaEventRecord(p->ev1, st);
         cudaError_t ce = cudaMemcpyAsync(h, p->d_slots, kNSlots * 8, cudaMemcpyDeviceToHost, st);
@@ -573,7 +591,7 @@ bdeg_status bdeg_finalize(bdeg_plan_t p, const int64_t *h_slots, bdeg_result *ou
         return BDEG_OK;
     }
     if (h_slots[SLOT_QFULL] > 0)
-        return fail(p, BDEG_E_TOO_LARGE, "overflow re-run queue exhausted; rerun with BDEG_FLAG_FORCE_TIER1");
+        return fail(p, BDEG_E_TOO_LARGE, "overflow re-run queue exhausted; rerun with BDEG_FLAG_FORCE_TIER2");
     bdeg_status s = slots_to_result(p, h_slots, &r);
     if (s) return s;
     *out = r;

@@ -12,6 +12,7 @@ typedef unsigned __int128 u128;
 
 constexpr int kMaxN = 64;    // points: the kernel maps one point to a lane slot (2 slots/lane)
 constexpr int kMaxK = 32;    // subset size (K+1 rows of the lifted matrix, <= 33)
+constexpr int kMaxInner = 6;   // register-resident DFS levels (template parameter S)
 constexpr int kBinomRows = 65;
 constexpr int kBinomCols = 34;
 
@@ -55,7 +56,8 @@ uint64_t derive_seed(uint64_t seed, int attempt);
 struct DeviceProblem {
     const int64_t *L;        // (K+1) x N lifted matrix, column-major: L[l*(K+1) + i]
     const uint64_t *binom;   // kBinomRows x kBinomCols
-    int K, N, S, T;          // subset size, points, inner levels, top (block) levels
+    int K, N, S, T;          // subset size, points, register-DFS levels, smem prefix levels (K-1-S)
+    int D;                   // work-item depth: items are D-tuples of the largest indices (D >= T)
 };
 
 struct LaunchArgs {
@@ -68,8 +70,9 @@ struct LaunchArgs {
     unsigned long long *ovf_queue;    // block ids whose int32-tier run overflowed
     unsigned long long *ovf_count;
     uint64_t ovf_cap;
-    int tier;                         // 0: int32 values / int64 products, 1: int64 / int128
-    int replay;                       // 1: process ovf_queue[0..*ovf_count) in tier 1
+    int tier;                         // 0: int32/int32, 1: int32/int64 (bounds), 2: int64/int128
+    int bits_v, bits_l;               // tier-1 bounds: |V| < 2^bits_v, |lift| < 2^bits_l
+    int replay;                       // 1: process ovf_queue[0..*ovf_count) in tier 2
     int grid, block;                  // launch shape
     void *stream;
 };

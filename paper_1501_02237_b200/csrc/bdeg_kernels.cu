@@ -36,16 +36,23 @@ uint64_t launch_counter_add(uint64_t k) { return g_launches.fetch_add(k) + k; }
 namespace dev {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kWarps = 8;           // warps per CTA
+constexpr int kWarps = 4;           // warps per CTA
 
-template <int TIER> struct VT;
-template <> struct VT<0> { typedef int32_t T; };
-template <> struct VT<1> { typedef int64_t T; };
+// Arithmetic tiers (value storage of the K "V" rows / of the lift row):
+//   0: int32 / int32, |v| < 2^31, products and numerators exact in int64
+//   1: int32 / int64, |V| < 2^Bv, |L| < 2^Bl with Bv + Bl <= 61 and
+//      2 Bv <= 61 (runtime bounds), numerators exact in int64
+//   2: int64 / int64, |v| < 2^62, numerators in int128, quotients verified
+// Tiers 0/1 check every stored value against its bound; a block that leaves
+// its tier is re-run in tier 2 (replay launch).
+template <int TIER> struct Tr;
+template <> struct Tr<0> { typedef int32_t VV; typedef int32_t VL; };
+template <> struct Tr<1> { typedef int32_t VV; typedef int64_t VL; };
+template <> struct Tr<2> { typedef int64_t VV; typedef int64_t VL; };
 
 // Exact division by a known divisor d != 0: shift out the 2-adic part, then
 // multiply by the inverse of the odd part mod 2^64.  Exact whenever the
-// dividend is a multiple of d and the quotient fits (Bareiss guarantees the
-// former; the callers check the latter).
+// dividend is a multiple of d (Bareiss guarantees it) and the quotient fits.
 struct Div {
     uint64_t inv;
     int64_t d;
@@ -57,26 +64,28 @@ __device__ __forceinline__ Div make_div(int64_t d) {
     Div r;
     r.d = d;
     r.unit = (d == 1) ? 1 : (d == -1 ? -1 : 0);
-    r.tz = __ffsll(d) - 1;
-    const uint64_t o = (uint64_t)(d >> r.tz);
-    uint64_t x = o;                        // correct to 3 bits
+    r.tz = 0;
+    r.inv = 1;
+    if (r.unit == 0) {
+        r.tz = __ffsll(d) - 1;
+        const uint64_t o = (uint64_t)(d >> r.tz);
+        uint64_t x = (3 * o) ^ 2;                      // correct to 5 bits
 #pragma unroll
-    for (int i = 0; i < 5; ++i) x *= 2 - o * x;   // Newton: 6, 12, 24, 48, 96 bits
-    r.inv = x;
+        for (int i = 0; i < 4; ++i) x *= 2 - o * x;    // 10, 20, 40, 80 bits
+        r.inv = x;
+    }
     return r;
 }
 
-// tier 0: |values| < 2^31, numerators exact in int64
 __device__ __forceinline__ int64_t qdiv64(int64_t num, const Div &dv) {
     if (dv.unit == 1) return num;
     if (dv.unit == -1) return -num;
     return (int64_t)((uint64_t)(num >> dv.tz) * dv.inv);
 }
-__device__ __forceinline__ bool fits31(int64_t v) {  // |v| <= 2^31 - 1
-    return (uint64_t)(v + 0x7FFFFFFFll) <= 0xFFFFFFFEull;
+// |v| < lim  (lim a power of two <= 2^62)
+__device__ __forceinline__ bool inside(int64_t v, int64_t lim) {
+    return (uint64_t)(v + (lim - 1)) <= (uint64_t)(2 * (lim - 1));
 }
-// tier 1: |values| < 2^62, numerators exact in int128; the quotient is
-// verified by multiplying back (detects any value beyond the int64 tier).
 __device__ __forceinline__ int64_t qdiv128(i128 num, const Div &dv, bool &ovf) {
     int64_t q;
     if (dv.unit != 0) {
@@ -87,8 +96,7 @@ __device__ __forceinline__ int64_t qdiv128(i128 num, const Div &dv, bool &ovf) {
         q = (int64_t)((uint64_t)(num >> dv.tz) * dv.inv);
         ovf |= ((i128)q * (i128)dv.d != num);
     }
-    const int64_t lim = (int64_t)1 << 62;
-    ovf |= (q >= lim) || (q <= -lim);
+    ovf |= !inside(q, (int64_t)1 << 62);
     return q;
 }
 
@@ -107,17 +115,25 @@ __device__ __forceinline__ uint32_t ford(float f) {
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+// Per-item accumulators (warp-uniform: every lane holds the same values).
 struct Acc {
-    uint64_t vol_lo, vol_hi, cells, singular, cand, ties, updates, leaves;
-    __device__ void zero() { vol_lo = vol_hi = cells = singular = cand = ties = updates = leaves = 0; }
+    uint64_t vol_lo, vol_hi, singular, cand, updates;
+    uint32_t cells, ties, leaves;
+    __device__ void zero() { vol_lo = vol_hi = singular = cand = updates = 0; cells = ties = leaves = 0; }
     __device__ void add_vol(uint64_t v) {
         uint64_t t = vol_lo + v;
         vol_hi += (t < vol_lo);
         vol_lo = t;
     }
+};
+// Per-warp totals.
+struct WAcc {
+    uint64_t vol_lo, vol_hi, cells, singular, cand, ties, updates, leaves;
+    __device__ void zero() { vol_lo = vol_hi = cells = singular = cand = ties = updates = leaves = 0; }
     __device__ void add(const Acc &o) {
-        add_vol(o.vol_lo);
-        vol_hi += o.vol_hi;
+        uint64_t t = vol_lo + o.vol_lo;
+        vol_hi += (t < vol_lo) + o.vol_hi;
+        vol_lo = t;
         cells += o.cells; singular += o.singular; cand += o.cand; ties += o.ties;
         updates += o.updates; leaves += o.leaves;
     }
@@ -127,6 +143,10 @@ struct Ctx {
     const uint64_t *B;   // binomial table in smem
     int N, K, lane;
     uint64_t rb, re;
+    int64_t limV, limL;  // tier-1 bounds (exclusive)
+    uint64_t nmask;      // points 0..N-1
+    int D, kd, fmin;     // item depth, K - D, smallest forced DFS level
+    int mytop;           // this lane's entry of the item tuple: c_{kd + lane} (lane < D)
     bool partial;
     __device__ __forceinline__ uint64_t C(int n, int k) const { return B[n * kBinomCols + k]; }
     // |[base, base+size) n [rb, re)|
@@ -139,12 +159,20 @@ struct Ctx {
 };
 
 // ------------------------------------------------------------------ leaf
-// x, y: leaf 2-vectors of this lane's points; c1 = smallest prefix index;
-// base = rank of candidate (j = 0, P); inP = prefix point mask; kappa = sign
-// of the last pivot.  Counts the candidates P u {j}, j in [0, c1) n range.
+// After the whole (K-1)-prefix P is eliminated every point l is a 2-vector
+// (x_l, y_l) = g * (+-det V_{P u l}, lift minor) for a common non-zero g.
+// With kappa = sign(last pivot) * sign(g), sigma = P u {j} is a cell iff
+//     sign(x_j) * (x_j * yk_l - x_l * yk_j) > 0   for every l not in sigma,
+// yk = kappa * y (DESIGN.md §"Leaf test").  So only the unique extreme
+// slopes yk/x of the half-planes x > 0 (min) and x < 0 (max) can be cells:
+// found with REDUX over approximate float keys (error << margin), then
+// verified exactly (int128) against every lane.  |det| = |x_j| / |g|.
+constexpr uint32_t kKeyMargin = 64;   // key units (ulps); the fp32 key error is < 8
+
 template <int NPL>
 __device__ __forceinline__ void leaf_test(const int64_t (&x)[NPL], const int64_t (&y)[NPL], int c1,
-                                          uint64_t base, uint64_t inP, int kappa, const Ctx &cx, Acc &acc) {
+                                          uint64_t base, uint64_t inP, int kappa, uint64_t gabs,
+                                          const Ctx &cx, Acc &acc) {
     int jlo = 0, jhi = c1;
     if (cx.partial) {
         if (cx.rb > base) jlo = (cx.rb - base >= (uint64_t)c1) ? c1 : (int)(cx.rb - base);
@@ -153,74 +181,55 @@ __device__ __forceinline__ void leaf_test(const int64_t (&x)[NPL], const int64_t
     }
     acc.cand += (uint64_t)(jhi - jlo);
     acc.leaves += 1;
+    // warp-uniform point masks: countable j in [jlo, jhi); valid l = not in P, < N
+    const uint64_t cntm = ((jhi >= 64) ? ~0ull : ((1ull << jhi) - 1)) & ~((1ull << jlo) - 1);
+    const uint64_t valm = ~inP & cx.nmask;
+    const uint32_t lanebit = 1u << cx.lane;
     int64_t yk[NPL];
-    bool valid[NPL], cnt[NPL];
-    bool bad0 = false, small = true, wide = false;
+    uint32_t kp = 0xFFFFFFFFu, km = 0xFFFFFFFFu;
+    uint32_t kq[NPL];
     unsigned sing = 0;
+    bool bad0 = false;
 #pragma unroll
     for (int q = 0; q < NPL; ++q) {
-        const int l = cx.lane + 32 * q;
-        valid[q] = (l < cx.N) && !((inP >> l) & 1ull);
-        cnt[q] = (l >= jlo) && (l < jhi);
+        const uint32_t vq = (uint32_t)(valm >> (32 * q));
+        const bool v = (vq & lanebit) != 0;
         yk[q] = kappa > 0 ? y[q] : -y[q];
-        sing += __popc(__ballot_sync(FULL, cnt[q] && x[q] == 0));
-        bad0 |= valid[q] && x[q] == 0 && yk[q] < 0;
-        const uint64_t ax = (uint64_t)(x[q] < 0 ? -x[q] : x[q]);
-        const uint64_t ay = (uint64_t)(yk[q] < 0 ? -yk[q] : yk[q]);
-        if (valid[q]) {
-            small &= (ax < (1ull << 24)) && (ay < (1ull << 24));
-            wide |= (ax >= (1ull << 53)) || (ay >= (1ull << 53));
-        }
+        const bool zx = x[q] == 0;
+        sing += __popc(__ballot_sync(FULL, zx) & (uint32_t)(cntm >> (32 * q)));
+        bad0 |= v && zx && yk[q] < 0;
+        // slope key yk/x (approximate; error << kKeyMargin key units)
+        const uint32_t o = ford(__fdividef((float)yk[q], (float)x[q]));
+        kq[q] = o;
+        if (v && x[q] > 0) kp = min(kp, o);
+        if (v && x[q] < 0) km = min(km, ~o);
     }
     acc.singular += sing;
-    if (__any_sync(FULL, bad0)) return;          // a point in span(P) strictly below
+    if (__any_sync(FULL, bad0)) return;          // a point of span(P) lies strictly below
+    const uint32_t mp = __reduce_min_sync(FULL, kp);   // ~ min slope over x > 0
+    const uint32_t mm = __reduce_min_sync(FULL, km);   // ~ max slope over x < 0 (complemented)
+    // both cells need  max_{x<0} slope < min_{x>0} slope
+    if (mp != 0xFFFFFFFFu && mm != 0xFFFFFFFFu && (~mm) > mp + 2 * kKeyMargin) return;
     uint64_t candmask = 0;
-    const bool anywide = __any_sync(FULL, wide);
-    if (!anywide) {
-        const bool allsmall = __all_sync(FULL, small);
-        uint32_t kp[NPL], km[NPL];
-        uint32_t mp = 0xFFFFFFFFu, mm = 0xFFFFFFFFu;
 #pragma unroll
-        for (int q = 0; q < NPL; ++q) {
-            kp[q] = km[q] = 0xFFFFFFFFu;
-            if (valid[q] && x[q] != 0) {
-                // slope y'/x, correctly rounded => monotone in the exact rational
-                float f = allsmall ? __fdiv_rn((float)yk[q], (float)x[q])
-                                   : __double2float_rn(__ddiv_rn((double)yk[q], (double)x[q]));
-                const uint32_t o = ford(f);
-                if (x[q] > 0) kp[q] = o; else km[q] = ~o;
-            }
-            mp = min(mp, kp[q]);
-            mm = min(mm, km[q]);
-        }
-        mp = __reduce_min_sync(FULL, mp);        // min slope over x > 0
-        mm = __reduce_min_sync(FULL, mm);        // max slope over x < 0 (complemented)
-        // both cells need  max_{x<0} slope < min_{x>0} slope ; float '>' is exact '>'
-        if (mp != 0xFFFFFFFFu && mm != 0xFFFFFFFFu && (~mm) > mp) return;
-#pragma unroll
-        for (int q = 0; q < NPL; ++q) {
-            const bool c = cnt[q] && ((kp[q] == mp && mp != 0xFFFFFFFFu) || (km[q] == mm && mm != 0xFFFFFFFFu));
-            candmask |= (uint64_t)__ballot_sync(FULL, c) << (32 * q);
-        }
-    } else {
-        // values beyond 2^53: no float keys, verify every countable j exactly
-#pragma unroll
-        for (int q = 0; q < NPL; ++q)
-            candmask |= (uint64_t)__ballot_sync(FULL, cnt[q] && x[q] != 0) << (32 * q);
+    for (int q = 0; q < NPL; ++q) {
+        const bool c = (x[q] > 0 && kq[q] <= mp + kKeyMargin) || (x[q] < 0 && (~kq[q]) <= mm + kKeyMargin);
+        candmask |= (uint64_t)__ballot_sync(FULL, c) << (32 * q);
     }
+    candmask &= cntm;
     while (candmask) {
         const int j = __ffsll((long long)candmask) - 1;
         candmask &= candmask - 1;
-        const int js = j >> 5, jl = j & 31;
+        const int jl = j & 31;
         int64_t xs = x[0], ys = yk[0];
-        if (NPL > 1 && js == 1) { xs = x[NPL - 1]; ys = yk[NPL - 1]; }
+        if (NPL > 1 && (j >> 5)) { xs = x[NPL - 1]; ys = yk[NPL - 1]; }
         const int64_t xj = shfl<int64_t>(xs, jl);
         const int64_t yj = shfl<int64_t>(ys, jl);
         bool bad = false, zero = false;
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
             const int l = cx.lane + 32 * q;
-            if (valid[q] && l != j) {
+            if (((valm >> l) & 1ull) && l != j) {
                 i128 c = (i128)xj * yk[q] - (i128)x[q] * yj;
                 if (xj < 0) c = -c;
                 bad |= c < 0;
@@ -232,200 +241,246 @@ __device__ __forceinline__ void leaf_test(const int64_t (&x)[NPL], const int64_t
             acc.ties += 1;                         // would-be cell on a tie (reading Z3)
         } else {
             acc.cells += 1;
-            acc.add_vol((uint64_t)(xj < 0 ? -xj : xj));   // |x_j| = |det V_sigma|
+            acc.add_vol((uint64_t)(xj < 0 ? -xj : xj) / gabs);   // |det V_sigma|
         }
     }
 }
 
-// --------------------------------------------------------- one elimination step
-// st: R rows (R-1 V rows, then the lift row) of this lane's points.  Pivot
-// column values colv (uniform), pivot row pr, pivot value piv, previous
-// pivot divisor dv.  Output: R-1 rows (other V rows in order, lift row last):
+// --------------------------------------------------------- elimination
+// State of this lane's points: sv[q][0..RV-1] (remaining V rows), sl[q] (lift).
+// Pivot column values cv[.], cl; pivot row pr; pivot piv; previous pivot dv:
 //     a'_{o,l} = (piv * a_{o,l} - a_{o,p} * a_{pr,l}) / prev      (Bareiss)
-template <int TIER, int NPL, int R, typename OT>
-__device__ __forceinline__ void elim_step(const typename VT<TIER>::T (&st)[NPL][R],
-                                          const typename VT<TIER>::T (&colv)[R], int pr,
-                                          typename VT<TIER>::T piv, const Div &dv,
-                                          OT (&out)[NPL][R - 1], bool &ovf) {
-    typedef typename VT<TIER>::T V;
+template <int TIER, int NPL, int RV>
+__device__ __forceinline__ void elim_step(const typename Tr<TIER>::VV (&sv)[NPL][RV],
+                                          const typename Tr<TIER>::VL (&sl)[NPL],
+                                          const typename Tr<TIER>::VV (&cv)[RV],
+                                          typename Tr<TIER>::VL cl, int pr, typename Tr<TIER>::VV piv,
+                                          const Div &dv, const Ctx &cx,
+                                          typename Tr<TIER>::VV (&ov)[NPL][RV - 1],
+                                          typename Tr<TIER>::VL (&ol)[NPL], bool &ovf) {
+    typedef typename Tr<TIER>::VV VV;
+    typedef typename Tr<TIER>::VL VL;
 #pragma unroll
     for (int q = 0; q < NPL; ++q) {
-        V prow = st[q][0];
+        VV prow = sv[q][0];
 #pragma unroll
-        for (int r = 1; r < R - 1; ++r) if (pr == r) prow = st[q][r];
+        for (int r = 1; r < RV; ++r) if (pr == r) prow = sv[q][r];
 #pragma unroll
-        for (int o = 0; o < R - 1; ++o) {
-            V s, cs;
-            if (o == R - 2) { s = st[q][R - 1]; cs = colv[R - 1]; }
-            else { s = (o < pr) ? st[q][o] : st[q][o + 1]; cs = (o < pr) ? colv[o] : colv[o + 1]; }
-            if constexpr (TIER == 0) {
-                const int64_t num = (int64_t)piv * (int64_t)s - (int64_t)cs * (int64_t)prow;
-                const int64_t v = qdiv64(num, dv);
-                if constexpr (sizeof(OT) == 4) ovf |= !fits31(v);
-                out[q][o] = (OT)v;
+        for (int o = 0; o < RV - 1; ++o) {
+            const VV s = (o < pr) ? sv[q][o] : sv[q][o + 1];
+            const VV cs = (o < pr) ? cv[o] : cv[o + 1];
+            if constexpr (TIER == 2) {
+                ov[q][o] = qdiv128((i128)piv * s - (i128)cs * prow, dv, ovf);
             } else {
-                const i128 num = (i128)piv * (i128)s - (i128)cs * (i128)prow;
-                out[q][o] = (OT)qdiv128(num, dv, ovf);
+                const int64_t v = qdiv64((int64_t)piv * s - (int64_t)cs * prow, dv);
+                ovf |= TIER == 0 ? !inside(v, (int64_t)1 << 31) : !inside(v, cx.limV);
+                ov[q][o] = (VV)v;
             }
+        }
+        if constexpr (TIER == 2) {
+            ol[q] = qdiv128((i128)piv * sl[q] - (i128)cl * prow, dv, ovf);
+        } else {
+            const int64_t v = qdiv64((int64_t)piv * (int64_t)sl[q] - (int64_t)cl * (int64_t)prow, dv);
+            ovf |= TIER == 0 ? !inside(v, (int64_t)1 << 31) : !inside(v, cx.limL);
+            ol[q] = (VL)v;
         }
     }
 }
 
-template <int TIER, int NPL, int R>
-__device__ __forceinline__ void fetch_col(const typename VT<TIER>::T (&st)[NPL][R], int c,
-                                          typename VT<TIER>::T (&colv)[R]) {
-    typedef typename VT<TIER>::T V;
+template <int TIER, int NPL, int RV>
+__device__ __forceinline__ void fetch_col(const typename Tr<TIER>::VV (&sv)[NPL][RV],
+                                          const typename Tr<TIER>::VL (&sl)[NPL], int c,
+                                          typename Tr<TIER>::VV (&cv)[RV], typename Tr<TIER>::VL &cl) {
+    typedef typename Tr<TIER>::VV VV;
+    typedef typename Tr<TIER>::VL VL;
     const int src = c & 31;
-    const bool hi = (c >> 5) != 0;
+    const bool hi = NPL > 1 && (c >> 5) != 0;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        V mine = st[0][r];
-        if (NPL > 1 && hi) mine = st[NPL - 1][r];
-        colv[r] = shfl<V>(mine, src);
-    }
+    for (int r = 0; r < RV; ++r) cv[r] = shfl<VV>(hi ? sv[NPL - 1][r] : sv[0][r], src);
+    cl = shfl<VL>(hi ? sl[NPL - 1] : sl[0], src);
 }
 
 // ------------------------------------------------------------ inner DFS
-// State with R >= 3 rows (R-1 remaining V rows + lift).  Chooses c_i,
-// i = R-2, in [i, cbound) in colex order; base = rank contribution of the
-// indices above; prev = previous pivot.
-template <int TIER, int NPL, int R>
-__device__ __forceinline__ void inner_dfs(const typename VT<TIER>::T (&st)[NPL][R], int cbound,
+// RV >= 2 remaining V rows.  Chooses c_i, i = RV-1, in [i, cbound) in colex
+// order; base = rank contribution of the indices above; prev = last pivot.
+template <int TIER, int NPL, int RV>
+__device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL][RV],
+                                          const typename Tr<TIER>::VL (&sl)[NPL], int cbound,
                                           uint64_t base, uint64_t inP, int64_t prev, const Ctx &cx,
                                           Acc &acc, bool &ovf) {
-    typedef typename VT<TIER>::T V;
-    constexpr int i = R - 2;
-    const Div dv = make_div(prev);
-    for (int c = i; c < cbound; ++c) {
+    typedef typename Tr<TIER>::VV VV;
+    typedef typename Tr<TIER>::VL VL;
+    constexpr int i = RV - 1;
+    Div dv;
+    if constexpr (RV > 2 || TIER == 2) dv = make_div(prev);
+    int lo = i, hi = cbound;
+    if (i >= cx.fmin) {                      // forced level: c_i is fixed by the work item
+        lo = __shfl_sync(FULL, cx.mytop, i - cx.kd);
+        hi = lo + 1;
+    }
+    for (int c = lo; c < hi; ++c) {
         const uint64_t nb = base + cx.C(c, i + 1);
         const uint64_t ns = cx.C(c, i);
         if (cx.partial && cx.isect(nb, ns) == 0) continue;
-        V colv[R];
-        fetch_col<TIER, NPL, R>(st, c, colv);
+        VV cv[RV];
+        VL cl;
+        fetch_col<TIER, NPL, RV>(sv, sl, c, cv, cl);
         int pr = -1;
 #pragma unroll
-        for (int r = R - 2; r >= 0; --r) if (colv[r] != 0) pr = r;
+        for (int r = RV - 1; r >= 0; --r) if (cv[r] != 0) pr = r;
         if (pr < 0) {                        // prefix dependent: whole subtree singular
             const uint64_t k = cx.isect(nb, ns);
             acc.singular += k;
             acc.cand += k;
             continue;
         }
-        V piv = colv[0];
+        VV piv = cv[0];
 #pragma unroll
-        for (int r = 1; r < R - 1; ++r) if (pr == r) piv = colv[r];
-        acc.updates += (uint64_t)(R - 1) * cx.N;
-        if constexpr (R == 3) {
-            int64_t out[NPL][2];
-            elim_step<TIER, NPL, R, int64_t>(st, colv, pr, piv, dv, out, ovf);
-            if constexpr (TIER == 1) {
-                if (__any_sync(FULL, ovf)) { ovf = true; return; }
-            }
+        for (int r = 1; r < RV; ++r) if (pr == r) piv = cv[r];
+        acc.updates += (uint64_t)RV * cx.N;
+        if constexpr (RV == 2) {
+            // last prefix index: the leaf 2-vectors
             int64_t xx[NPL], yy[NPL];
+            const VV cs = pr == 0 ? cv[1] : cv[0];
+            if constexpr (TIER == 2) {
 #pragma unroll
-            for (int q = 0; q < NPL; ++q) { xx[q] = out[q][0]; yy[q] = out[q][1]; }
-            leaf_test<NPL>(xx, yy, c, nb, inP | (1ull << c), piv > 0 ? 1 : -1, cx, acc);
+                for (int q = 0; q < NPL; ++q) {
+                    const VV prow = pr == 0 ? sv[q][0] : sv[q][1];
+                    const VV s = pr == 0 ? sv[q][1] : sv[q][0];
+                    xx[q] = qdiv128((i128)piv * s - (i128)cs * prow, dv, ovf);
+                    yy[q] = qdiv128((i128)piv * sl[q] - (i128)cl * prow, dv, ovf);
+                }
+                if (__any_sync(FULL, ovf)) { ovf = true; return; }
+                leaf_test<NPL>(xx, yy, c, nb, inP | (1ull << c), piv > 0 ? 1 : -1, 1, cx, acc);
+            } else {
+                // no division: (x, y) = prev * (true values); exact in int64
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) {
+                    const VV prow = pr == 0 ? sv[q][0] : sv[q][1];
+                    const VV s = pr == 0 ? sv[q][1] : sv[q][0];
+                    xx[q] = (int64_t)piv * s - (int64_t)cs * prow;
+                    yy[q] = (int64_t)piv * (int64_t)sl[q] - (int64_t)cl * (int64_t)prow;
+                }
+                const int kappa = ((piv > 0) == (prev > 0)) ? 1 : -1;
+                leaf_test<NPL>(xx, yy, c, nb, inP | (1ull << c), kappa,
+                               (uint64_t)(prev < 0 ? -prev : prev), cx, acc);
+            }
         } else {
-            V out[NPL][R - 1];
-            elim_step<TIER, NPL, R, V>(st, colv, pr, piv, dv, out, ovf);
+            VV ov[NPL][RV - 1];
+            VL ol[NPL];
+            elim_step<TIER, NPL, RV>(sv, sl, cv, cl, pr, piv, dv, cx, ov, ol, ovf);
             if (__any_sync(FULL, ovf)) { ovf = true; return; }
-            inner_dfs<TIER, NPL, R - 1>(out, c, nb, inP | (1ull << c), (int64_t)piv, cx, acc, ovf);
+            inner_dfs<TIER, NPL, RV - 1>(ov, ol, c, nb, inP | (1ull << c), (int64_t)piv, cx, acc, ovf);
             if (ovf) return;
         }
     }
 }
 
-// ------------------------------------------------------------ one block
-// Block id -> top tuple (colex over T-subsets of {0..N-S-2}, shifted by S+1),
-// prefix elimination in shared scratch, then the register DFS.
+// ------------------------------------------------------------ one work item
+// Item id -> D-tuple (c_{K-D} < ... < c_{K-1}) by colex unranking over
+// D-subsets of {0..N-K+D-1} shifted by K-D.  The T = K-1-S largest entries
+// are eliminated in shared scratch (tier-2 arithmetic); the other D-T are
+// "forced" levels of the S-level register DFS, which walks the rest.
 template <int TIER, int NPL, int S>
-__device__ void process_block(uint64_t blk, const int64_t *Lsm, int64_t *scr, const Ctx &cx0,
-                              int T, Acc &acc, bool &ovf) {
-    typedef typename VT<TIER>::T V;
+__device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, const Ctx &cx0,
+                             Acc &acc, bool &ovf) {
+    typedef typename Tr<TIER>::VV VV;
+    typedef typename Tr<TIER>::VL VL;
     const int lane = cx0.lane;
-    const int K = cx0.K, N = cx0.N;
+    const int K = cx0.K, N = cx0.N, D = cx0.D, kd = cx0.kd;
     constexpr int NP = 32 * NPL;
-    // --- unrank the top tuple: lane t (< T) holds c_{S+1+t}
+    const int T = K - 1 - S;
+    // --- unrank: lane t (< D) holds c_{kd+t}
     int mytop = 0;
     {
-        uint64_t r = blk;
-        for (int t = T - 1; t >= 0; --t) {
-            // largest u with C(u, t+1) <= r  (u < N-S-1)
-            uint32_t m0 = __ballot_sync(FULL, lane < N - S - 1 && cx0.C(lane, t + 1) <= r);
-            uint32_t m1 = __ballot_sync(FULL, lane + 32 < N - S - 1 && cx0.C(lane + 32, t + 1) <= r);
+        uint64_t r = item;
+        const int M = N - kd;                 // u ranges over [0, M)
+        for (int t = D - 1; t >= 0; --t) {
+            const uint32_t m0 = __ballot_sync(FULL, lane < M && cx0.C(lane, t + 1) <= r);
+            const uint32_t m1 = __ballot_sync(FULL, lane + 32 < M && cx0.C(lane + 32, t + 1) <= r);
             const int u = m1 ? 32 + 31 - __clz(m1) : 31 - __clz(m0);
             r -= cx0.C(u, t + 1);
-            if (lane == t) mytop = u + S + 1;
+            if (lane == t) mytop = u + kd;
         }
     }
-    // rank base and size of the block
-    uint64_t term = (lane < T) ? cx0.C(mytop, S + 2 + lane) : 0;
+    // item rank range: sum over all D entries; size C(c_{kd}, kd)
+    uint64_t tall = (lane < D) ? cx0.C(mytop, kd + lane + 1) : 0;
+    uint64_t ttop = (lane < D && lane >= D - T) ? tall : 0;    // the T smem entries only
 #pragma unroll
-    for (int o = 16; o; o >>= 1) term += __shfl_xor_sync(FULL, term, o);
-    const uint64_t bbase = term;
-    const int ctop = T > 0 ? __shfl_sync(FULL, mytop, 0) : N;
-    const uint64_t bsize = cx0.C(ctop, S + 1);
+    for (int o = 16; o; o >>= 1) {
+        tall += __shfl_xor_sync(FULL, tall, o);
+        ttop += __shfl_xor_sync(FULL, ttop, o);
+    }
+    const int cfirst = D > 0 ? __shfl_sync(FULL, mytop, 0) : N;
+    const uint64_t isize = cx0.C(cfirst, kd);
     Ctx cx = cx0;
+    cx.mytop = mytop;
     {
-        const uint64_t lo = bbase > cx0.rb ? bbase : cx0.rb;
-        const uint64_t hi = bbase + bsize < cx0.re ? bbase + bsize : cx0.re;
+        // effective range = item n [rb, re).  Forced levels' subtrees span
+        // other items too, so with forced levels every count is clamped here.
+        const uint64_t lo = tall > cx0.rb ? tall : cx0.rb;
+        const uint64_t hi = tall + isize < cx0.re ? tall + isize : cx0.re;
         if (hi <= lo) return;
-        cx.partial = (lo != bbase) || (hi != bbase + bsize);
+        cx.rb = lo;
+        cx.re = hi;
+        cx.partial = (lo != tall) || (hi != tall + isize) || (D > T);
     }
     uint64_t inP = 0;
     {
-        const uint64_t bit = (lane < T) ? (1ull << mytop) : 0ull;
+        const uint64_t bit = (lane < D && lane >= D - T) ? (1ull << mytop) : 0ull;
         const unsigned lo = __reduce_or_sync(FULL, (unsigned)bit);
         const unsigned hi = __reduce_or_sync(FULL, (unsigned)(bit >> 32));
         inP = ((uint64_t)hi << 32) | lo;
     }
-    // --- prefix elimination in shared scratch: scr[i*NP + l], rows 0..K
-    __syncwarp();
-    for (int i = 0; i <= K; ++i)
-#pragma unroll
-        for (int q = 0; q < NPL; ++q) {
-            const int l = lane + 32 * q;
-            scr[i * NP + l] = (l < N) ? Lsm[l * (K + 1) + i] : 0;
-        }
-    __syncwarp();
-    uint64_t alive = (K >= 64) ? ~0ull : ((1ull << K) - 1);
+    // --- elimination of the T largest entries in shared scratch: scr[i*NP + l], rows 0..K
     int64_t prev = 1;
-    for (int t = 0; t < T; ++t) {
-        const int p = __shfl_sync(FULL, mytop, T - 1 - t);   // pivot order c_{K-1}, c_{K-2}, ...
-        const bool nz = (lane < K) && ((alive >> lane) & 1ull) && scr[lane * NP + p] != 0;
-        const unsigned bal = __ballot_sync(FULL, nz);
-        if (bal == 0) {                                       // dependent block prefix
-            const uint64_t k = cx.isect(bbase, bsize);
-            acc.singular += k;
-            acc.cand += k;
-            return;
-        }
-        const int r = __ffs(bal) - 1;
-        const int64_t piv = scr[r * NP + p];
-        const Div dv = make_div(prev);
-        bool o = false;
-        for (int i = 0; i <= K; ++i) {
-            if (i == r || (i < K && !((alive >> i) & 1ull))) continue;
-            const int64_t ci = scr[i * NP + p];
+    uint64_t alive = (1ull << K) - 1;
+    if (T > 0) {
+        __syncwarp();
+        for (int i = 0; i <= K; ++i)
 #pragma unroll
             for (int q = 0; q < NPL; ++q) {
                 const int l = lane + 32 * q;
-                if (l == p) continue;
-                const i128 num = (i128)piv * scr[i * NP + l] - (i128)ci * scr[r * NP + l];
-                const int64_t v = qdiv128(num, dv, o);
-                scr[i * NP + l] = v;
+                scr[i * NP + l] = (l < N) ? Lsm[l * (K + 1) + i] : 0;
             }
-        }
-        acc.updates += (uint64_t)(K - t) * N;
-        if (__any_sync(FULL, o)) { ovf = true; return; }     // beyond the int64 tier
-        alive &= ~(1ull << r);
-        prev = piv;
         __syncwarp();
+        for (int t = 0; t < T; ++t) {
+            const int p = __shfl_sync(FULL, mytop, D - 1 - t);   // pivot order c_{K-1}, c_{K-2}, ...
+            const bool nz = (lane < K) && ((alive >> lane) & 1ull) && scr[lane * NP + p] != 0;
+            const unsigned bal = __ballot_sync(FULL, nz);
+            if (bal == 0) {                                       // dependent prefix
+                const uint64_t k = cx.isect(tall, isize);
+                acc.singular += k;
+                acc.cand += k;
+                return;
+            }
+            const int r = __ffs(bal) - 1;
+            const int64_t piv = scr[r * NP + p];
+            const Div dv = make_div(prev);
+            bool o = false;
+            for (int i = 0; i <= K; ++i) {
+                if (i == r || (i < K && !((alive >> i) & 1ull))) continue;
+                const int64_t ci = scr[i * NP + p];
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) {
+                    const int l = lane + 32 * q;
+                    if (l == p) continue;
+                    const i128 num = (i128)piv * scr[i * NP + l] - (i128)ci * scr[r * NP + l];
+                    scr[i * NP + l] = qdiv128(num, dv, o);
+                }
+            }
+            acc.updates += (uint64_t)(K - t) * N;
+            if (__any_sync(FULL, o)) { ovf = true; return; }     // beyond the int64 tier
+            alive &= ~(1ull << r);
+            prev = piv;
+            __syncwarp();
+        }
     }
     // --- registers: remaining S+1 V rows (ascending) then the lift row
-    V st[NPL][S + 2];
+    VV sv[NPL][S + 1];
+    VL sl[NPL];
     bool o = false;
-    {
+    if (T > 0) {
         int k = 0;
         for (int i = 0; i < K; ++i) {
             if (!((alive >> i) & 1ull)) continue;
@@ -435,27 +490,47 @@ __device__ void process_block(uint64_t blk, const int64_t *Lsm, int64_t *scr, co
 #pragma unroll
                     for (int q = 0; q < NPL; ++q) {
                         const int64_t v = scr[i * NP + lane + 32 * q];
-                        if (TIER == 0) o |= !fits31(v);
-                        st[q][kk] = (V)v;
+                        if constexpr (TIER == 0) o |= !inside(v, (int64_t)1 << 31);
+                        if constexpr (TIER == 1) o |= !inside(v, cx.limV);
+                        sv[q][kk] = (VV)v;
                     }
             ++k;
         }
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
             const int64_t v = scr[K * NP + lane + 32 * q];
-            if (TIER == 0) o |= !fits31(v);
-            st[q][S + 1] = (V)v;
+            if constexpr (TIER == 0) o |= !inside(v, (int64_t)1 << 31);
+            if constexpr (TIER == 1) o |= !inside(v, cx.limL);
+            sl[q] = (VL)v;
+        }
+    } else {                                   // S = K-1: straight from the staged matrix
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const int l = lane + 32 * q;
+#pragma unroll
+            for (int kk = 0; kk < S + 1; ++kk) {
+                const int64_t v = (l < N) ? Lsm[l * (K + 1) + kk] : 0;
+                if constexpr (TIER == 0) o |= !inside(v, (int64_t)1 << 31);
+                if constexpr (TIER == 1) o |= !inside(v, cx.limV);
+                sv[q][kk] = (VV)v;
+            }
+            const int64_t v = (l < N) ? Lsm[l * (K + 1) + K] : 0;
+            if constexpr (TIER == 0) o |= !inside(v, (int64_t)1 << 31);
+            if constexpr (TIER == 1) o |= !inside(v, cx.limL);
+            sl[q] = (VL)v;
         }
     }
     if (__any_sync(FULL, o)) { ovf = true; return; }
+    const int ctop = T > 0 ? __shfl_sync(FULL, mytop, D - T) : N;   // c_{S+1}
     if constexpr (S == 0) {
-        // the block is a single leaf: prefix = the top tuple, c1 = ctop
+        // the item is a single leaf: prefix = the tuple, c1 = ctop; the
+        // shared-memory values are the true minors (divided), so g = 1
         int64_t xx[NPL], yy[NPL];
 #pragma unroll
-        for (int q = 0; q < NPL; ++q) { xx[q] = (int64_t)st[q][0]; yy[q] = (int64_t)st[q][S + 1]; }
-        leaf_test<NPL>(xx, yy, ctop, bbase, inP, prev > 0 ? 1 : -1, cx, acc);
+        for (int q = 0; q < NPL; ++q) { xx[q] = (int64_t)sv[q][0]; yy[q] = (int64_t)sl[q]; }
+        leaf_test<NPL>(xx, yy, ctop, ttop, inP, prev > 0 ? 1 : -1, 1, cx, acc);
     } else {
-        inner_dfs<TIER, NPL, S + 2>(st, ctop, bbase, inP, prev, cx, acc, ovf);
+        inner_dfs<TIER, NPL, S + 1>(sv, sl, ctop, ttop, inP, prev, cx, acc, ovf);
     }
 }
 
@@ -465,10 +540,16 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 }
 
 template <int TIER, int NPL, int S>
-__global__ void __launch_bounds__(kWarps * 32)
+// Occupancy: deep register DFS (S >= 5) gets <= 168 registers (3 CTAs of 4
+// warps per SM), otherwise <= 128 (4 CTAs); measured best on B200.
+#ifndef BDEG_MIN_BLOCKS
+#define BDEG_MIN_BLOCKS (S >= 5 ? 3 : 4)
+#endif
+__global__ void __launch_bounds__(kWarps * 32, BDEG_MIN_BLOCKS)
 k_enumerate(LaunchArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int K = a.P.K, N = a.P.N, T = a.P.T;
+    (void)T;
     const uint32_t lbytes = (uint32_t)(((K + 1) * N * 8 + 15) & ~15);
     const uint32_t bbytes = kBinomRows * kBinomCols * 8;
     int64_t *Lsm = reinterpret_cast<int64_t *>(smem);
@@ -517,9 +598,16 @@ k_enumerate(LaunchArgs a) {
     cx.rb = a.rank_begin;
     cx.re = a.rank_end;
     cx.partial = true;
+    cx.limV = (int64_t)1 << a.bits_v;
+    cx.limL = (int64_t)1 << a.bits_l;
+    cx.nmask = (N >= 64) ? ~0ull : ((1ull << N) - 1);
     int64_t *scr = scr_all + (size_t)warp * (K + 1) * 32 * NPL;
 
-    Acc wacc;
+    cx.D = a.P.D;
+    cx.kd = K - a.P.D;
+    cx.fmin = (a.P.D > T) ? K - a.P.D : S + 1;
+    cx.mytop = 0;
+    WAcc wacc;
     wacc.zero();
     unsigned long long n_ovf = 0, n_fatal = 0, n_qfull = 0, n_blocks = 0;
     const uint64_t span = a.blk_last - a.blk_first + 1;
@@ -534,11 +622,11 @@ k_enumerate(LaunchArgs a) {
         Acc bacc;
         bacc.zero();
         bool ovf = false;
-        process_block<TIER, NPL, S>(blk, Lsm, scr, cx, T, bacc, ovf);
+        process_item<TIER, NPL, S>(blk, Lsm, scr, cx, bacc, ovf);
         ovf = __any_sync(FULL, ovf);
         ++n_blocks;
         if (ovf) {
-            if (TIER == 0) {
+            if (TIER != 2) {
                 ++n_ovf;
                 if (lane == 0) {
                     const unsigned long long pos = atomicAdd(a.ovf_count, 1ull);
@@ -599,10 +687,10 @@ typedef void (*KernFn)(LaunchArgs);
 static KernFn pick(int tier, int npl, int S) {
 #define BDEG_K(T_, P_, S_) \
     if (tier == T_ && npl == P_ && S == S_) return dev::k_enumerate<T_, P_, S_>;
-    BDEG_K(0, 1, 0) BDEG_K(0, 1, 1) BDEG_K(0, 1, 2) BDEG_K(0, 1, 3)
-    BDEG_K(0, 2, 0) BDEG_K(0, 2, 1) BDEG_K(0, 2, 2) BDEG_K(0, 2, 3)
-    BDEG_K(1, 1, 0) BDEG_K(1, 1, 1) BDEG_K(1, 1, 2) BDEG_K(1, 1, 3)
-    BDEG_K(1, 2, 0) BDEG_K(1, 2, 1) BDEG_K(1, 2, 2) BDEG_K(1, 2, 3)
+#define BDEG_KS(T_, P_) BDEG_K(T_, P_, 0) BDEG_K(T_, P_, 1) BDEG_K(T_, P_, 2) BDEG_K(T_, P_, 3) \
+    BDEG_K(T_, P_, 4) BDEG_K(T_, P_, 5) BDEG_K(T_, P_, 6)
+    BDEG_KS(0, 1) BDEG_KS(0, 2) BDEG_KS(1, 1) BDEG_KS(1, 2) BDEG_KS(2, 1) BDEG_KS(2, 2)
+#undef BDEG_KS
 #undef BDEG_K
     return nullptr;
 }

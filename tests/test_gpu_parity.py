@@ -79,7 +79,7 @@ def test_toric_closed_forms():
 
 
 @pytest.mark.parametrize("inner", [0, 1, 2, 3])
-@pytest.mark.parametrize("tierflag", [0x4, 0x8])
+@pytest.mark.parametrize("tierflag", [0x4, 0x8, 0x20])
 def test_inner_levels_and_tiers(inner, tierflag):
     # every register-DFS depth and both arithmetic tiers give identical counts
     for (n_pts, dim, seed) in [(14, 4, 1), (33, 3, 2), (40, 4, 3), (64, 3, 4)]:
@@ -92,7 +92,7 @@ def test_inner_levels_and_tiers(inner, tierflag):
 
 def test_tier0_overflow_rerun():
     # raw SNF basis of C2 needs > 31-bit values: the int32 tier must hand the
-    # affected blocks to the int64 tier and still be exact
+    # affected blocks to tier 2 and still be exact
     A, b, lift = W.c2_system(5)
     o, _ = _oracle_system(A, b, lift)
     r = B.Plan.from_system(A, b, lift, flags=0x1 | 0x4, inner_levels=0).degree()

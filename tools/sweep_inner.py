@@ -1,0 +1,33 @@
+#!/usr/bin/env python
+"""Sweep the register-DFS depth S (inner_levels) on a few workloads; prints ms and rate."""
+import json
+import math
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1501_02237_b200 as B  # noqa: E402
+
+wls = sys.argv[1].split(",") if len(sys.argv) > 1 else ["c5", "w25", "w26"]
+Ss = [int(s) for s in sys.argv[2].split(",")] if len(sys.argv) > 2 else [2, 3, 4, 5, 6]
+torch.cuda.set_device(0)
+for wl in wls:
+    desc, K, V, w, extra = bench.workload(wl)
+    total = math.comb(len(V), K)
+    for S in Ss:
+        if S > K - 1:
+            continue
+        p = B.Plan.from_points(V, w, inner_levels=S)
+        r = p.degree()   # warm
+        reps = 3 if total < 1e10 else 1
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r = p.degree()
+        dt = (time.perf_counter() - t0) / reps
+        print(json.dumps({"wl": wl, "S": S, "tier": r.tier, "ms": dt * 1e3, "kernel_ms": r.kernel_ms,
+                          "rate": total / dt, "degree": r.degree, "leaves": r.leaves}), flush=True)
+        p.close()
