@@ -143,6 +143,19 @@ bdeg_status bdeg_degree(bdeg_plan_t plan, bdeg_result *out);
  * C(c_i, i+1), c_0 < ... < c_{K-1}); no re-lift (ties are reported). */
 bdeg_status bdeg_degree_range(bdeg_plan_t plan, uint64_t begin, uint64_t end, bdeg_result *out);
 
+/* Work decomposition of the rank space (host only).  Item i is a tuple of
+ * the largest subset indices; its candidates are the contiguous colex ranks
+ * [*begin, *end).  Items partition [0, C(N,K)).  Sharding rule of
+ * bdeg_degree_partial: rank r of world W takes the items i with
+ * (num_items - 1 - i) mod W == r (largest items first). */
+uint64_t bdeg_num_items(bdeg_plan_t plan);
+bdeg_status bdeg_item_range(bdeg_plan_t plan, uint64_t item, uint64_t *begin, uint64_t *end);
+
+/* Result slots (int64, summed by the all-reduce): [0..3] the degree as four
+ * 32-bit limbs (value = sum_i slot[i] << 32i), [4] cells, [5] singular,
+ * [6] candidates, [7] ties, [8] blocks re-run in tier 2, [9] tier-2 overflow
+ * (fatal), [10] re-run queue exhausted, [11] items, [12] updates, [13] leaves. */
+
 /* This process's shard (options.rank of options.world) accumulated into the
  * caller's DEVICE buffer d_slots (BDEG_NSLOTS int64, zeroed here), async on
  * the stream.  Combine with one all-reduce(SUM) and call bdeg_finalize. */

@@ -79,7 +79,8 @@ class _Result(ctypes.Structure):
 EXPORTS = ["bdeg_default_options", "bdeg_plan", "bdeg_plan_points", "bdeg_plan_info",
            "bdeg_workspace_bytes", "bdeg_set_workspace", "bdeg_degree", "bdeg_degree_range",
            "bdeg_degree_partial", "bdeg_finalize", "bdeg_relift", "bdeg_last_error",
-           "bdeg_status_str", "bdeg_destroy", "bdeg_launch_count"]
+           "bdeg_status_str", "bdeg_destroy", "bdeg_launch_count", "bdeg_num_items",
+           "bdeg_item_range"]
 
 
 def _load():
@@ -109,6 +110,10 @@ def _load():
     lib.bdeg_status_str.restype = ctypes.c_char_p
     lib.bdeg_destroy.argtypes = [plan_t]
     lib.bdeg_destroy.restype = None
+    lib.bdeg_num_items.argtypes = [plan_t]
+    lib.bdeg_num_items.restype = ctypes.c_uint64
+    lib.bdeg_item_range.argtypes = [plan_t, ctypes.c_uint64, P(ctypes.c_uint64), P(ctypes.c_uint64)]
+    lib.bdeg_item_range.restype = ctypes.c_int
     lib.bdeg_launch_count.argtypes = []
     lib.bdeg_launch_count.restype = ctypes.c_uint64
     for name in ["bdeg_plan", "bdeg_plan_points", "bdeg_plan_info", "bdeg_set_workspace",
@@ -261,6 +266,19 @@ class Plan:
         r = _Result()
         _check(lib.bdeg_plan_info(self._h, ctypes.byref(r)), self._h)
         return _result(r)
+
+    def num_items(self) -> int:
+        return int(lib.bdeg_num_items(self._h))
+
+    def item_range(self, item: int):
+        b, e = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib.bdeg_item_range(self._h, item, ctypes.byref(b), ctypes.byref(e)), self._h)
+        return b.value, e.value
+
+    def shard_items(self, rank: int, world: int):
+        """Items of `rank` under bdeg_degree_partial's sharding rule."""
+        n = self.num_items()
+        return [n - 1 - (rank + i * world) for i in range((n - rank + world - 1) // world) if n - 1 - (rank + i * world) >= 0]
 
     def workspace_bytes(self) -> int:
         return int(lib.bdeg_workspace_bytes(self._h))

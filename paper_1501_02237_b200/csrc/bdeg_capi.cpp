@@ -598,6 +598,27 @@ bdeg_status bdeg_finalize(bdeg_plan_t p, const int64_t *h_slots, bdeg_result *ou
     return BDEG_OK;
 }
 
+uint64_t bdeg_num_items(bdeg_plan_t p) { return (p && p->K > 0) ? p->nblocks : 0; }
+
+bdeg_status bdeg_item_range(bdeg_plan_t p, uint64_t item, uint64_t *begin, uint64_t *end) {
+    if (!p || !begin || !end) return fail(p, BDEG_E_INVALID, "NULL argument");
+    if (p->K == 0 || item >= p->nblocks) return fail(p, BDEG_E_INVALID, "item out of range");
+    // colex unrank of the item over D-subsets of {0..N-K+D-1}, shifted by K-D
+    const int D = p->D, kd = p->K - p->D;
+    uint64_t r = item, base = 0;
+    int first = p->N;
+    for (int t = D - 1; t >= 0; --t) {
+        int u = t;
+        while (C(p->binom, u + 1, t + 1) <= r) ++u;
+        r -= C(p->binom, u, t + 1);
+        base += C(p->binom, u + kd, kd + t + 1);
+        if (t == 0) first = u + kd;
+    }
+    *begin = base;
+    *end = base + C(p->binom, first, kd);
+    return BDEG_OK;
+}
+
 const char *bdeg_last_error(bdeg_plan_t p) { return p ? p->err.c_str() : g_err.c_str(); }
 
 const char *bdeg_status_str(bdeg_status s) {

@@ -28,3 +28,15 @@ def table3():
             m, k, v, kind = line.split()
             out[(int(m), int(k))] = (int(v), kind)
     return out
+
+
+def _ensure_built():
+    """The C ABI library is an in-tree nvcc build (git-ignored); build it if a
+    fresh checkout lacks it (nvcc cross-compiles for sm_100a without a GPU)."""
+    lib = os.path.join(ROOT, "paper_1501_02237_b200", "libbdeg.so")
+    if not os.path.exists(lib):
+        from paper_1501_02237_b200._build import build_lib
+        build_lib()
+
+
+_ensure_built()

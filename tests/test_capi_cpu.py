@@ -1,0 +1,133 @@
+"""CPU-side checks of the C ABI (no GPU): the library loads, exports every
+entry point include/bdeg.h declares, its host front end agrees with the
+oracle, and device entry points fail loudly instead of falling back."""
+import ctypes
+import math
+import os
+import re
+
+import pytest
+
+import workloads as W
+from oracle import analyze, point_configuration
+
+import paper_1501_02237_b200 as B
+from paper_1501_02237_b200 import bdeg as BB
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "bdeg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bdeg_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    names = _declared()
+    assert len(names) >= 15
+    lib = ctypes.CDLL(B.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(BB.EXPORTS)
+
+
+def test_built_for_sm100a():
+    out = os.popen(f"cuobjdump --list-elf {B.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("mk", [(1, 2), (2, 2), (2, 3), (3, 3), (2, 4), (3, 4), (4, 4), (2, 7), (4, 5)])
+def test_front_end_matches_oracle_master_space(mk):
+    A, b = W.master_space_system(*mk)
+    lift = W.liftings(len(A) + 1, 1)
+    cfg = point_configuration(A, b, lift)
+    info = B.Plan.from_system(A, b, lift).info()
+    assert (info.rank, info.dim, info.components) == (cfg["rank"], cfg["dim"], cfg["components"])
+    K, V, w = cfg["cone"]
+    assert (info.K, info.N, info.homogeneous) == (K, len(V), True)
+    assert info.total_candidates == math.comb(len(V), K)
+
+
+@pytest.mark.parametrize("seed", [5, 31, 46, 66])
+def test_front_end_matches_oracle_c2(seed):
+    A, b, lift = W.c2_system(seed)
+    cfg = point_configuration(A, b, lift)
+    for flags in (0, BB.FLAG_NO_LLL):
+        info = B.Plan.from_system(A, b, lift, flags=flags).info()
+        assert info.components == cfg["components"] == 2
+        assert (info.K, info.N, info.homogeneous) == (5, 13, False)
+
+
+def test_front_end_other_systems():
+    for sysf in [W.twisted_cubic_system(), W.conifold_system(), W.dp0_system(), W.segre_system(2, 3),
+                 W.veronese_system(2, 3), W.rnc_system(9)]:
+        A, b = sysf
+        cfg = point_configuration(A, b, W.liftings(len(A) + 1, 1))
+        info = B.Plan.from_system(A, b).info()
+        assert (info.dim, info.components) == (cfg["dim"], cfg["components"])
+        K, V, _ = cfg["cone"]
+        assert (info.K, info.N) == (K, len(V))
+
+
+def test_no_homog_shortcut_flag():
+    A, b = W.master_space_system(2, 2)
+    info = B.Plan.from_system(A, b, flags=BB.FLAG_NO_HOMOG_SHORTCUT).info()
+    assert (info.K, info.N, info.homogeneous) == (7, 13, False)
+
+
+def test_inconsistent_and_dimension_zero():
+    with pytest.raises(B.BdegError) as ei:
+        B.Plan.from_system([[1, 1], [0, 0]], [1, 2])
+    assert ei.value.status == BB.BDEG_E_INCONSISTENT
+    r = B.degree([[2, 0], [0, 3]])          # d = 0: no device work
+    assert (r.dim, r.degree, r.components) == (0, 1, 6)
+    assert analyze([[2, 0], [0, 3]])["components"] == 6
+
+
+def test_limits_and_bad_args():
+    V, w = W.c5_points(1, n_points=40, dim=7)
+    with pytest.raises(B.BdegError) as ei:
+        B.Plan.from_points([(1,) + (0,) * 40] * 41, None)      # K = 41 > 32
+    assert ei.value.status == BB.BDEG_E_TOO_LARGE
+    with pytest.raises(B.BdegError) as ei:
+        B.Plan.from_points(V[:5], w[:5])                          # N < K
+    assert ei.value.status == BB.BDEG_E_INVALID
+
+
+def test_items_partition_rank_space():
+    for (V, w, K) in [(W.c5_points(1)[0], W.c5_points(1)[1], 8),
+                      (W.c5_points(2, n_points=20, dim=3)[0], None, 4)]:
+        p = B.Plan.from_points(V, w)
+        n = p.num_items()
+        rs = sorted(p.item_range(i) for i in range(n))
+        assert rs[0][0] == 0 and rs[-1][1] == math.comb(len(V), K)
+        assert all(rs[i][1] == rs[i + 1][0] for i in range(n - 1))
+        shards = [set(p.shard_items(r, 3)) for r in range(3)]
+        assert set().union(*shards) == set(range(n)) and sum(map(len, shards)) == n
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    A, b = W.master_space_system(2, 2)
+    with pytest.raises(B.BdegError) as ei:
+        B.degree(A, b)
+    assert ei.value.status == BB.BDEG_E_CUDA
+
+
+def test_finalize_exact_limbs():
+    from paper_1501_02237_b200.multi import pack_slots
+    p = B.Plan.from_points(*W.c5_points(1, n_points=12, dim=3))
+    big = (1 << 100) + 12345678901234567
+    r = p.finalize(pack_slots(big, 7, 8, 9))
+    assert (r.degree, r.cells, r.singular, r.candidates) == (big, 7, 8, 9)
+    # limbs summed across ranks without carries (a limb slot may exceed 2^32)
+    s1 = pack_slots((1 << 40) - 1, 1, 0, 5)
+    s2 = pack_slots((1 << 40) - 1, 2, 0, 6)
+    tot = [a + b for a, b in zip(s1, s2)]
+    assert p.finalize(tot).degree == 2 * ((1 << 40) - 1)

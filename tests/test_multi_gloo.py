@@ -1,0 +1,78 @@
+"""World-size-2 test of the multi-GPU path on CPU (gloo): each rank plans the
+same problem deterministically, computes its interleaved share of the work
+items (here with the CPU oracle standing in for the GPU kernel), packs the
+16 result slots, one all-reduce(SUM) combines them, and bdeg_finalize (the
+C ABI's host-side combine) must give the full-rank-space result."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import workloads as W
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cases, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1501_02237_b200 as B
+    from paper_1501_02237_b200.multi import all_reduce_slots, pack_slots
+    from oracle.native import enumerate_range
+    out = []
+    for (V, w, K) in cases:
+        plan = B.Plan.from_points(V, w, rank=rank, world=world)
+        # the plan is replicated: every rank must see the same decomposition
+        n = torch.tensor([plan.num_items()], dtype=torch.int64)
+        mx = n.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        assert int(mx) == int(n)
+        acc = {"volume": 0, "cells": 0, "singular": 0, "candidates": 0, "ties": 0}
+        for it in plan.shard_items(rank, world):
+            b, e = plan.item_range(it)
+            r = enumerate_range(K, V, w, b, e)
+            for k in acc:
+                acc[k] += r[k]
+        slots = torch.tensor(pack_slots(acc["volume"], acc["cells"], acc["singular"],
+                                        acc["candidates"], acc["ties"]), dtype=torch.int64)
+        all_reduce_slots(slots)
+        res = plan.finalize(slots.tolist())
+        out.append((res.degree, res.cells, res.singular, res.candidates))
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_combine_gloo(world):
+    cases = []
+    V, w = W.c5_points(3, n_points=14, dim=4)
+    cases.append((V, w, 5))
+    from oracle import point_configuration
+    A, b = W.master_space_system(2, 2)
+    K, V2, w2 = point_configuration(A, b, W.liftings(len(A) + 1, 1))["cone"]
+    cases.append((V2, w2, K))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    from oracle.native import enumerate_range
+    for i, (V, w, K) in enumerate(cases):
+        full = enumerate_range(K, V, w)
+        want = (full["volume"], full["cells"], full["singular"], full["candidates"])
+        assert res[0][i] == res[1][i] == want
+    assert res[0][1][0] == 14          # W_{2,2}: Table 3
