@@ -147,6 +147,7 @@ struct Ctx {
     uint64_t nmask;      // points 0..N-1
     int D, kd, fmin;     // item depth, K - D, smallest forced DFS level
     int mytop;           // this lane's entry of the item tuple: c_{kd + lane} (lane < D)
+    uint64_t irb, ire;   // the item's candidates n [rb, re)
     bool partial;
     __device__ __forceinline__ uint64_t C(int n, int k) const { return B[n * kBinomCols + k]; }
     // |[base, base+size) n [rb, re)|
@@ -300,6 +301,117 @@ __device__ __forceinline__ void fetch_col(const typename Tr<TIER>::VV (&sv)[NPL]
     cl = shfl<VL>(hi ? sl[NPL - 1] : sl[0], src);
 }
 
+// ------------------------------------------------------------ leaf level
+// Tiers 0/1: the DFS level that picks c_1 (two V rows u, v and the lift z
+// remain) fused with the leaf test.  For pivot point c the leaf 2-vectors are
+//   X_l = piv*s_l - cs*prow_l,   Y_l = kappa'*(piv*z_l - z_c*prow_l)
+// (prow = pivot row, s = the other V row), i.e. prev * (true Bareiss values):
+// no division is needed, since slopes and cross-product signs are invariant
+// under the common factor prev, whose sign is folded into kappa'
+// (= sign(piv) * sign(prev)).  |det| = |X_j| / |prev| for the (rare) cells.
+template <int TIER, int NPL>
+__device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL][2],
+                                           const typename Tr<TIER>::VL (&sl)[NPL], int lo, int hi,
+                                           uint64_t base, uint64_t inP, int64_t prev, const Ctx &cx,
+                                           Acc &acc) {
+    typedef typename Tr<TIER>::VV VV;
+    typedef typename Tr<TIER>::VL VL;
+    const uint64_t gabs = (uint64_t)(prev < 0 ? -prev : prev);
+    const bool gneg = prev < 0;
+    const uint32_t lanebit = 1u << cx.lane;
+    const uint64_t vbase = ~inP & cx.nmask;
+    for (int c = lo; c < hi; ++c) {
+        const uint64_t nb = base + (uint64_t)c * (uint64_t)(c - 1) / 2;   // + C(c, 2)
+        int jlo = 0, jhi = c;
+        if (cx.partial) {
+            if (cx.irb > nb) jlo = (cx.irb - nb >= (uint64_t)c) ? c : (int)(cx.irb - nb);
+            if (cx.ire < nb + (uint64_t)c) jhi = (cx.ire <= nb) ? 0 : (int)(cx.ire - nb);
+            if (jlo >= jhi) continue;
+        }
+        const int src = c & 31;
+        const bool hs = NPL > 1 && (c >> 5) != 0;
+        const VV u = shfl<VV>(hs ? sv[NPL - 1][0] : sv[0][0], src);
+        const VV v = shfl<VV>(hs ? sv[NPL - 1][1] : sv[0][1], src);
+        const VL z = shfl<VL>(hs ? sl[NPL - 1] : sl[0], src);
+        acc.cand += (uint64_t)(jhi - jlo);
+        acc.leaves += 1;
+        acc.updates += 2ull * cx.N;
+        if (u == 0 && v == 0) {                    // dependent prefix: every j singular
+            acc.singular += (uint64_t)(jhi - jlo);
+            continue;
+        }
+        const bool p0 = u != 0;
+        const VV piv = p0 ? u : v;
+        const VV cs = p0 ? v : u;
+        const bool kneg = (piv < 0) != gneg;
+        const VV pz = kneg ? (VV)-piv : piv;
+        const VL cz = kneg ? (VL)-z : z;
+        const uint64_t vm = vbase & ~(1ull << c);
+        const uint64_t cm = ((1ull << jhi) - 1) & ~((1ull << jlo) - 1);   // jhi <= c <= 63
+        int64_t X[NPL], Y[NPL];
+        float fx[NPL];
+        uint32_t key[NPL];
+        uint32_t kp = 0xFFFFFFFFu, km = 0xFFFFFFFFu;
+        unsigned sing = 0;
+        bool bad0 = false;
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const VV prow = p0 ? sv[q][0] : sv[q][1];
+            const VV s = p0 ? sv[q][1] : sv[q][0];
+            X[q] = (int64_t)piv * s - (int64_t)cs * prow;
+            Y[q] = (int64_t)pz * (int64_t)sl[q] - (int64_t)cz * (int64_t)prow;
+            fx[q] = (float)X[q];
+            const float fy = (float)Y[q];
+            const bool val = ((uint32_t)(vm >> (32 * q)) & lanebit) != 0;
+            sing += __popc(__ballot_sync(FULL, fx[q] == 0.0f) & (uint32_t)(cm >> (32 * q)));
+            bad0 |= val && fx[q] == 0.0f && fy < 0.0f;
+            const uint32_t o = ford(__fdividef(fy, fx[q]));
+            key[q] = o;
+            if (val && fx[q] > 0.0f) kp = min(kp, o);
+            if (val && fx[q] < 0.0f) km = min(km, ~o);
+        }
+        acc.singular += sing;
+        if (__any_sync(FULL, bad0)) continue;      // a point of span(P) lies strictly below
+        const uint32_t mp = __reduce_min_sync(FULL, kp);   // ~ min slope over x > 0
+        const uint32_t mm = __reduce_min_sync(FULL, km);   // ~ max slope over x < 0 (complemented)
+        if (mp != 0xFFFFFFFFu && mm != 0xFFFFFFFFu && (~mm) > mp + 2 * kKeyMargin) continue;
+        uint64_t candmask = 0;
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const bool cd = (fx[q] > 0.0f && key[q] <= mp + kKeyMargin) ||
+                            (fx[q] < 0.0f && (~key[q]) <= mm + kKeyMargin);
+            candmask |= (uint64_t)__ballot_sync(FULL, cd) << (32 * q);
+        }
+        candmask &= cm;
+        while (candmask) {                         // exact verification (int128)
+            const int j = __ffsll((long long)candmask) - 1;
+            candmask &= candmask - 1;
+            const int jl = j & 31;
+            const bool js = NPL > 1 && (j >> 5) != 0;
+            const int64_t xj = shfl<int64_t>(js ? X[NPL - 1] : X[0], jl);
+            const int64_t yj = shfl<int64_t>(js ? Y[NPL - 1] : Y[0], jl);
+            bool bad = false, zero = false;
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int l = cx.lane + 32 * q;
+                if (((vm >> l) & 1ull) && l != j) {
+                    i128 cr = (i128)xj * Y[q] - (i128)X[q] * yj;
+                    if (xj < 0) cr = -cr;
+                    bad |= cr < 0;
+                    zero |= cr == 0;
+                }
+            }
+            if (__any_sync(FULL, bad)) continue;
+            if (__any_sync(FULL, zero)) {
+                acc.ties += 1;                     // would-be cell on a tie (reading Z3)
+            } else {
+                acc.cells += 1;
+                acc.add_vol((uint64_t)(xj < 0 ? -xj : xj) / gabs);   // |det V_sigma|
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------ inner DFS
 // RV >= 2 remaining V rows.  Chooses c_i, i = RV-1, in [i, cbound) in colex
 // order; base = rank contribution of the indices above; prev = last pivot.
@@ -311,13 +423,17 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
     typedef typename Tr<TIER>::VV VV;
     typedef typename Tr<TIER>::VL VL;
     constexpr int i = RV - 1;
-    Div dv;
-    if constexpr (RV > 2 || TIER == 2) dv = make_div(prev);
     int lo = i, hi = cbound;
     if (i >= cx.fmin) {                      // forced level: c_i is fixed by the work item
         lo = __shfl_sync(FULL, cx.mytop, i - cx.kd);
         hi = lo + 1;
     }
+    if constexpr (RV == 2 && TIER != 2) {
+        leaf_level<TIER, NPL>(sv, sl, lo, hi, base, inP, prev, cx, acc);
+        return;
+    }
+    Div dv;
+    if constexpr (RV > 2 || TIER == 2) dv = make_div(prev);
     for (int c = lo; c < hi; ++c) {
         const uint64_t nb = base + cx.C(c, i + 1);
         const uint64_t ns = cx.C(c, i);
@@ -329,7 +445,7 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
 #pragma unroll
         for (int r = RV - 1; r >= 0; --r) if (cv[r] != 0) pr = r;
         if (pr < 0) {                        // prefix dependent: whole subtree singular
-            const uint64_t k = cx.isect(nb, ns);
+            const uint64_t k = (i >= cx.fmin) ? cx.ire - cx.irb : cx.isect(nb, ns);
             acc.singular += k;
             acc.cand += k;
             continue;
@@ -342,7 +458,7 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
             // last prefix index: the leaf 2-vectors
             int64_t xx[NPL], yy[NPL];
             const VV cs = pr == 0 ? cv[1] : cv[0];
-            if constexpr (TIER == 2) {
+            {
 #pragma unroll
                 for (int q = 0; q < NPL; ++q) {
                     const VV prow = pr == 0 ? sv[q][0] : sv[q][1];
@@ -352,18 +468,6 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
                 }
                 if (__any_sync(FULL, ovf)) { ovf = true; return; }
                 leaf_test<NPL>(xx, yy, c, nb, inP | (1ull << c), piv > 0 ? 1 : -1, 1, cx, acc);
-            } else {
-                // no division: (x, y) = prev * (true values); exact in int64
-#pragma unroll
-                for (int q = 0; q < NPL; ++q) {
-                    const VV prow = pr == 0 ? sv[q][0] : sv[q][1];
-                    const VV s = pr == 0 ? sv[q][1] : sv[q][0];
-                    xx[q] = (int64_t)piv * s - (int64_t)cs * prow;
-                    yy[q] = (int64_t)piv * (int64_t)sl[q] - (int64_t)cl * (int64_t)prow;
-                }
-                const int kappa = ((piv > 0) == (prev > 0)) ? 1 : -1;
-                leaf_test<NPL>(xx, yy, c, nb, inP | (1ull << c), kappa,
-                               (uint64_t)(prev < 0 ? -prev : prev), cx, acc);
             }
         } else {
             VV ov[NPL][RV - 1];
@@ -416,14 +520,14 @@ __device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, co
     Ctx cx = cx0;
     cx.mytop = mytop;
     {
-        // effective range = item n [rb, re).  Forced levels' subtrees span
-        // other items too, so with forced levels every count is clamped here.
+        // effective range = item n [rb, re).  A forced level's subtree spans
+        // other items too: its dependent-prefix count is clamped to [irb, ire).
         const uint64_t lo = tall > cx0.rb ? tall : cx0.rb;
         const uint64_t hi = tall + isize < cx0.re ? tall + isize : cx0.re;
         if (hi <= lo) return;
-        cx.rb = lo;
-        cx.re = hi;
-        cx.partial = (lo != tall) || (hi != tall + isize) || (D > T);
+        cx.irb = lo;
+        cx.ire = hi;
+        cx.partial = (lo != tall) || (hi != tall + isize);
     }
     uint64_t inP = 0;
     {
