@@ -309,6 +309,33 @@ __device__ __forceinline__ void fetch_col(const typename Tr<TIER>::VV (&sv)[NPL]
 // no division is needed, since slopes and cross-product signs are invariant
 // under the common factor prev, whose sign is folded into kappa'
 // (= sign(piv) * sign(prev)).  |det| = |X_j| / |prev| for the (rare) cells.
+__device__ __forceinline__ float rcp_approx(float x) {   // MUFU.RCP, |x| >= 1 here
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// signed 32 x 32 -> 64 (IMAD.WIDE) and multiply-add
+__device__ __forceinline__ int64_t mulw(int32_t a, int32_t b) {
+    int64_t r;
+    asm("mul.wide.s32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ int64_t madw(int32_t a, int32_t b, int64_t c) {
+    int64_t r;
+    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+    return r;
+}
+// a float the compiler cannot trace back to its integer source (keeps the
+// sign tests as single FSETPs instead of 64-bit integer compares)
+__device__ __forceinline__ float opaque(float x) {
+    float r;
+    asm("mov.b32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float unford(uint32_t o) {   // inverse of ford
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+}
+
 template <int TIER, int NPL>
 __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL][2],
                                            const typename Tr<TIER>::VL (&sl)[NPL], int lo, int hi,
@@ -318,71 +345,89 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
     typedef typename Tr<TIER>::VL VL;
     const uint64_t gabs = (uint64_t)(prev < 0 ? -prev : prev);
     const bool gneg = prev < 0;
-    const uint32_t lanebit = 1u << cx.lane;
-    const uint64_t vbase = ~inP & cx.nmask;
+    const float INFF = __int_as_float(0x7f800000);
+    // lanes holding a point that is not in the parent prefix (fixed for the loop)
+    bool vpar[NPL];
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) {
+        const int l = cx.lane + 32 * q;
+        vpar[q] = l < cx.N && !((inP >> l) & 1ull);
+    }
+    if (!cx.partial && hi > lo) {              // whole leaves: counters per parent
+        const uint64_t nl = (uint64_t)(hi - lo);
+        acc.leaves += (uint32_t)nl;
+        acc.updates += 2ull * cx.N * nl;
+        acc.cand += ((uint64_t)hi * (hi - 1) - (uint64_t)lo * (lo - 1)) / 2;   // sum of c
+    }
     for (int c = lo; c < hi; ++c) {
-        const uint64_t nb = base + (uint64_t)c * (uint64_t)(c - 1) / 2;   // + C(c, 2)
         int jlo = 0, jhi = c;
+        uint64_t nb = 0;
         if (cx.partial) {
+            nb = base + (uint64_t)c * (uint64_t)(c - 1) / 2;   // + C(c, 2)
             if (cx.irb > nb) jlo = (cx.irb - nb >= (uint64_t)c) ? c : (int)(cx.irb - nb);
             if (cx.ire < nb + (uint64_t)c) jhi = (cx.ire <= nb) ? 0 : (int)(cx.ire - nb);
             if (jlo >= jhi) continue;
+            acc.cand += (uint64_t)(jhi - jlo);
+            acc.leaves += 1;
+            acc.updates += 2ull * cx.N;
         }
         const int src = c & 31;
         const bool hs = NPL > 1 && (c >> 5) != 0;
         const VV u = shfl<VV>(hs ? sv[NPL - 1][0] : sv[0][0], src);
         const VV v = shfl<VV>(hs ? sv[NPL - 1][1] : sv[0][1], src);
         const VL z = shfl<VL>(hs ? sl[NPL - 1] : sl[0], src);
-        acc.cand += (uint64_t)(jhi - jlo);
-        acc.leaves += 1;
-        acc.updates += 2ull * cx.N;
         if (u == 0 && v == 0) {                    // dependent prefix: every j singular
             acc.singular += (uint64_t)(jhi - jlo);
             continue;
         }
         const bool p0 = u != 0;
         const VV piv = p0 ? u : v;
-        const VV cs = p0 ? v : u;
+        const VV ncs = p0 ? -v : -u;               // -(pivot column entry of the other row)
         const bool kneg = (piv < 0) != gneg;
         const VV pz = kneg ? (VV)-piv : piv;
-        const VL cz = kneg ? (VL)-z : z;
-        const uint64_t vm = vbase & ~(1ull << c);
-        const uint64_t cm = ((1ull << jhi) - 1) & ~((1ull << jlo) - 1);   // jhi <= c <= 63
+        const VL ncz = kneg ? z : (VL)-z;
         int64_t X[NPL], Y[NPL];
-        float fx[NPL];
-        uint32_t key[NPL];
-        uint32_t kp = 0xFFFFFFFFu, km = 0xFFFFFFFFu;
-        unsigned sing = 0;
+        float fx[NPL], key[NPL];
+        float fp = INFF, fm = INFF;
         bool bad0 = false;
+        unsigned sing = 0;
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
+            const int l = cx.lane + 32 * q;
             const VV prow = p0 ? sv[q][0] : sv[q][1];
             const VV s = p0 ? sv[q][1] : sv[q][0];
-            X[q] = (int64_t)piv * s - (int64_t)cs * prow;
-            Y[q] = (int64_t)pz * (int64_t)sl[q] - (int64_t)cz * (int64_t)prow;
-            fx[q] = (float)X[q];
-            const float fy = (float)Y[q];
-            const bool val = ((uint32_t)(vm >> (32 * q)) & lanebit) != 0;
-            sing += __popc(__ballot_sync(FULL, fx[q] == 0.0f) & (uint32_t)(cm >> (32 * q)));
-            bad0 |= val && fx[q] == 0.0f && fy < 0.0f;
-            const uint32_t o = ford(__fdividef(fy, fx[q]));
-            key[q] = o;
-            if (val && fx[q] > 0.0f) kp = min(kp, o);
-            if (val && fx[q] < 0.0f) km = min(km, ~o);
+            X[q] = madw(piv, s, mulw(ncs, prow));
+            if constexpr (TIER == 0) Y[q] = madw(pz, sl[q], mulw(ncz, prow));
+            else Y[q] = (int64_t)pz * (int64_t)sl[q] + (int64_t)ncz * (int64_t)prow;
+            fx[q] = opaque((float)X[q]);
+            const float fy = opaque((float)Y[q]);
+            const bool val = vpar[q] && l != c;
+            const bool cnt = l >= jlo && l < jhi;
+            const bool zer = fx[q] == 0.0f;
+            sing += __popc(__ballot_sync(FULL, cnt && zer));
+            bad0 |= val && zer && fy < 0.0f;
+            key[q] = fy * rcp_approx(fx[q]);       // slope, |error| << kKeyMargin units
+            fp = fminf(fp, (val && fx[q] > 0.0f) ? key[q] : INFF);
+            fm = fminf(fm, (val && fx[q] < 0.0f) ? -key[q] : INFF);
         }
         acc.singular += sing;
-        if (__any_sync(FULL, bad0)) continue;      // a point of span(P) lies strictly below
-        const uint32_t mp = __reduce_min_sync(FULL, kp);   // ~ min slope over x > 0
-        const uint32_t mm = __reduce_min_sync(FULL, km);   // ~ max slope over x < 0 (complemented)
-        if (mp != 0xFFFFFFFFu && mm != 0xFFFFFFFFu && (~mm) > mp + 2 * kKeyMargin) continue;
+        // a point of span(P) strictly below rejects the leaf: force key 0 (no real key is 0)
+        const uint32_t mp = __reduce_min_sync(FULL, bad0 ? 0u : ford(fp));   // ~ min slope, x > 0
+        const uint32_t mm = __reduce_min_sync(FULL, bad0 ? 0u : ford(fm));   // ~ -max slope, x < 0
+        if (mp == 0u || mm == 0u) continue;
+        const uint32_t INF = 0xFF800000u;                  // ford(+inf): group empty
+        // both cells need  max_{x<0} slope < min_{x>0} slope; ford(-x) = ~ford(x)
+        if (mp != INF && mm != INF && (~mm) > mp + 2 * kKeyMargin) continue;
+        const float tp = mp == INF ? -INFF : unford(mp + kKeyMargin);
+        const float tm = mm == INF ? -INFF : unford(mm + kKeyMargin);
         uint64_t candmask = 0;
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
-            const bool cd = (fx[q] > 0.0f && key[q] <= mp + kKeyMargin) ||
-                            (fx[q] < 0.0f && (~key[q]) <= mm + kKeyMargin);
+            const int l = cx.lane + 32 * q;
+            const bool cnt = l >= jlo && l < jhi;
+            const bool cd = cnt && ((fx[q] > 0.0f && key[q] <= tp) || (fx[q] < 0.0f && -key[q] <= tm));
             candmask |= (uint64_t)__ballot_sync(FULL, cd) << (32 * q);
         }
-        candmask &= cm;
         while (candmask) {                         // exact verification (int128)
             const int j = __ffsll((long long)candmask) - 1;
             candmask &= candmask - 1;
@@ -394,7 +439,7 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
 #pragma unroll
             for (int q = 0; q < NPL; ++q) {
                 const int l = cx.lane + 32 * q;
-                if (((vm >> l) & 1ull) && l != j) {
+                if (vpar[q] && l != c && l != j) {
                     i128 cr = (i128)xj * Y[q] - (i128)X[q] * yj;
                     if (xj < 0) cr = -cr;
                     bad |= cr < 0;
