@@ -82,6 +82,22 @@ __device__ __forceinline__ int64_t qdiv64(int64_t num, const Div &dv) {
     if (dv.unit == -1) return -num;
     return (int64_t)((uint64_t)(num >> dv.tz) * dv.inv);
 }
+// Exact quotient known to fit int32 (tiers 0/1, V rows): only the low word
+// of (num >> tz) times the odd inverse is needed; one wide multiply-back
+// verifies the result (flags any quotient outside int32, or INT32_MIN).
+__device__ __forceinline__ int32_t qdiv32(int64_t num, const Div &dv, bool &ovf) {
+    int32_t q;
+    if (dv.unit != 0) {
+        const int64_t t = dv.unit > 0 ? num : -num;
+        q = (int32_t)t;
+        ovf |= (int64_t)q != t;
+    } else {
+        q = (int32_t)((uint32_t)(num >> dv.tz) * (uint32_t)dv.inv);
+        ovf |= (int64_t)q * dv.d != num;
+    }
+    ovf |= q == INT32_MIN;
+    return q;
+}
 // |v| < lim  (lim a power of two <= 2^62)
 __device__ __forceinline__ bool inside(int64_t v, int64_t lim) {
     return (uint64_t)(v + (lim - 1)) <= (uint64_t)(2 * (lim - 1));
@@ -113,6 +129,33 @@ __device__ __forceinline__ int64_t shfl<int64_t>(int64_t v, int src) {
 __device__ __forceinline__ uint32_t ford(float f) {
     uint32_t b = __float_as_uint(f);
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {   // MUFU.RCP, |x| >= 1 here
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// signed 32 x 32 -> 64 (IMAD.WIDE) and multiply-add
+__device__ __forceinline__ int64_t mulw(int32_t a, int32_t b) {
+    int64_t r;
+    asm("mul.wide.s32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ int64_t madw(int32_t a, int32_t b, int64_t c) {
+    int64_t r;
+    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+    return r;
+}
+// a float the compiler cannot trace back to its integer source (keeps the
+// sign tests as single FSETPs instead of 64-bit integer compares)
+__device__ __forceinline__ float opaque(float x) {
+    float r;
+    asm("mov.b32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float unford(uint32_t o) {   // inverse of ford
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
 }
 
 // Per-item accumulators (warp-uniform: every lane holds the same values).
@@ -272,17 +315,21 @@ __device__ __forceinline__ void elim_step(const typename Tr<TIER>::VV (&sv)[NPL]
             const VV cs = (o < pr) ? cv[o] : cv[o + 1];
             if constexpr (TIER == 2) {
                 ov[q][o] = qdiv128((i128)piv * s - (i128)cs * prow, dv, ovf);
+            } else if constexpr (TIER == 0) {
+                ov[q][o] = qdiv32(madw(piv, s, mulw(-cs, prow)), dv, ovf);
             } else {
-                const int64_t v = qdiv64((int64_t)piv * s - (int64_t)cs * prow, dv);
-                ovf |= TIER == 0 ? !inside(v, (int64_t)1 << 31) : !inside(v, cx.limV);
-                ov[q][o] = (VV)v;
+                const int32_t v = qdiv32(madw(piv, s, mulw(-cs, prow)), dv, ovf);
+                ovf |= !inside(v, cx.limV);
+                ov[q][o] = v;
             }
         }
         if constexpr (TIER == 2) {
             ol[q] = qdiv128((i128)piv * sl[q] - (i128)cl * prow, dv, ovf);
+        } else if constexpr (TIER == 0) {
+            ol[q] = qdiv32(madw(piv, sl[q], mulw(-cl, prow)), dv, ovf);
         } else {
             const int64_t v = qdiv64((int64_t)piv * (int64_t)sl[q] - (int64_t)cl * (int64_t)prow, dv);
-            ovf |= TIER == 0 ? !inside(v, (int64_t)1 << 31) : !inside(v, cx.limL);
+            ovf |= !inside(v, cx.limL);
             ol[q] = (VL)v;
         }
     }
@@ -309,33 +356,6 @@ __device__ __forceinline__ void fetch_col(const typename Tr<TIER>::VV (&sv)[NPL]
 // no division is needed, since slopes and cross-product signs are invariant
 // under the common factor prev, whose sign is folded into kappa'
 // (= sign(piv) * sign(prev)).  |det| = |X_j| / |prev| for the (rare) cells.
-__device__ __forceinline__ float rcp_approx(float x) {   // MUFU.RCP, |x| >= 1 here
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-// signed 32 x 32 -> 64 (IMAD.WIDE) and multiply-add
-__device__ __forceinline__ int64_t mulw(int32_t a, int32_t b) {
-    int64_t r;
-    asm("mul.wide.s32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
-    return r;
-}
-__device__ __forceinline__ int64_t madw(int32_t a, int32_t b, int64_t c) {
-    int64_t r;
-    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
-    return r;
-}
-// a float the compiler cannot trace back to its integer source (keeps the
-// sign tests as single FSETPs instead of 64-bit integer compares)
-__device__ __forceinline__ float opaque(float x) {
-    float r;
-    asm("mov.b32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ float unford(uint32_t o) {   // inverse of ford
-    return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
-}
-
 template <int TIER, int NPL>
 __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL][2],
                                            const typename Tr<TIER>::VL (&sl)[NPL], int lo, int hi,
@@ -517,10 +537,10 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
         } else {
             VV ov[NPL][RV - 1];
             VL ol[NPL];
+            // overflow is voted once per item (the item is discarded and replayed);
+            // loops are index-bounded, so garbage values cannot hang the warp
             elim_step<TIER, NPL, RV>(sv, sl, cv, cl, pr, piv, dv, cx, ov, ol, ovf);
-            if (__any_sync(FULL, ovf)) { ovf = true; return; }
             inner_dfs<TIER, NPL, RV - 1>(ov, ol, c, nb, inP | (1ull << c), (int64_t)piv, cx, acc, ovf);
-            if (ovf) return;
         }
     }
 }
