@@ -69,6 +69,10 @@ typedef struct {
 #define BDEG_FLAG_FORCE_TIER1       0x8u  /* start in tier 1: int32 V rows / int64 lift row, int64 products */
 #define BDEG_FLAG_FORCE_TIER2       0x20u /* tier 2 only: int64 values, checked int128 products       */
 #define BDEG_FLAG_NO_RELIFT         0x10u /* report BDEG_E_DEGENERATE instead of re-lifting       */
+#define BDEG_FLAG_DEGREE_ONLY       0x40u /* skip cell-dead subtrees (a point of the prefix span
+                                             lies strictly below: no cell); degree,
+                                             cells, candidates stay exact, singular becomes a
+                                             lower bound (singular_complete = 0)              */
 
 typedef struct {
     uint64_t seed;           /* seed of the generated lifting (and of re-lifts)      */
@@ -99,8 +103,10 @@ typedef struct {
     uint64_t overflow_reruns;/* blocks re-run in tier 2 after leaving their tier     */
     uint64_t updates;        /* fraction-free elimination updates executed          */
     uint64_t leaves;         /* (K-1)-prefixes tested (each = one warp-wide facet test) */
+    uint64_t dead_leaves;    /* of which inside cell-dead subtrees (singular count only) */
     int32_t relifts;         /* re-lift attempts used                                */
     int32_t consistent;      /* 0 if b^{Q_0} != 1                                    */
+    int32_t singular_complete; /* 1 unless BDEG_FLAG_DEGREE_ONLY                      */
     uint64_t seed_used;      /* seed of the lifting that produced the result         */
     uint64_t total_candidates; /* C(N,K)                                             */
     double plan_ms, kernel_ms, total_ms;
@@ -154,7 +160,8 @@ bdeg_status bdeg_item_range(bdeg_plan_t plan, uint64_t item, uint64_t *begin, ui
 /* Result slots (int64, summed by the all-reduce): [0..3] the degree as four
  * 32-bit limbs (value = sum_i slot[i] << 32i), [4] cells, [5] singular,
  * [6] candidates, [7] ties, [8] blocks re-run in tier 2, [9] tier-2 overflow
- * (fatal), [10] re-run queue exhausted, [11] items, [12] updates, [13] leaves. */
+ * (fatal), [10] re-run queue exhausted, [11] items, [12] updates, [13] leaves,
+ * [14] dead leaves. */
 
 /* This process's shard (options.rank of options.world) accumulated into the
  * caller's DEVICE buffer d_slots (BDEG_NSLOTS int64, zeroed here), async on

@@ -33,6 +33,7 @@ FLAG_FORCE_TIER0 = 0x4
 FLAG_FORCE_TIER1 = 0x8
 FLAG_NO_RELIFT = 0x10
 FLAG_FORCE_TIER2 = 0x20
+FLAG_DEGREE_ONLY = 0x40
 TIER_DTYPE = {0: "int32", 1: "int32/int64", 2: "int64/int128"}
 
 NSLOTS = 16
@@ -69,8 +70,10 @@ class _Result(ctypes.Structure):
                 ("candidates", ctypes.c_uint64), ("cells", ctypes.c_uint64),
                 ("singular", ctypes.c_uint64), ("ties", ctypes.c_uint64),
                 ("overflow_reruns", ctypes.c_uint64), ("updates", ctypes.c_uint64),
-                ("leaves", ctypes.c_uint64), ("relifts", ctypes.c_int32),
-                ("consistent", ctypes.c_int32), ("seed_used", ctypes.c_uint64),
+                ("leaves", ctypes.c_uint64), ("dead_leaves", ctypes.c_uint64),
+                ("relifts", ctypes.c_int32),
+                ("consistent", ctypes.c_int32), ("singular_complete", ctypes.c_int32),
+                ("seed_used", ctypes.c_uint64),
                 ("total_candidates", ctypes.c_uint64),
                 ("plan_ms", ctypes.c_double), ("kernel_ms", ctypes.c_double),
                 ("total_ms", ctypes.c_double)]
@@ -149,8 +152,10 @@ class Result:
     overflow_reruns: int
     updates: int
     leaves: int
+    dead_leaves: int
     relifts: int
     consistent: bool
+    singular_complete: bool
     seed_used: int
     total_candidates: int
     plan_ms: float
@@ -166,8 +171,10 @@ def _result(r: _Result) -> Result:
                   homogeneous=bool(r.homogeneous), inner_levels=r.inner_levels,
                   components=comps, degree=deg, candidates=r.candidates, cells=r.cells,
                   singular=r.singular, ties=r.ties, overflow_reruns=r.overflow_reruns,
-                  updates=r.updates, leaves=r.leaves, relifts=r.relifts,
-                  consistent=bool(r.consistent), seed_used=r.seed_used,
+                  updates=r.updates, leaves=r.leaves, dead_leaves=r.dead_leaves,
+                  relifts=r.relifts,
+                  consistent=bool(r.consistent), singular_complete=bool(r.singular_complete),
+                  seed_used=r.seed_used,
                   total_candidates=r.total_candidates, plan_ms=r.plan_ms,
                   kernel_ms=r.kernel_ms, total_ms=r.total_ms)
 

@@ -313,6 +313,7 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     a.stream = st;
     a.tier = force_tier >= 0 ? force_tier : p->tier;
     a.bits_v = p->bits_v;
+    a.degree_only = (p->opt.flags & BDEG_FLAG_DEGREE_ONLY) ? 1 : 0;
     a.bits_l = p->bits_l;
     a.replay = 0;
     a.counter = p->d_ctr + 0;
@@ -342,6 +343,7 @@ void fill_front(const bdeg_plan_s *p, bdeg_result *r) {
     r->comp_hi = p->points_mode ? 0 : (uint64_t)(p->fe.components >> 64);
     r->consistent = p->points_mode ? 1 : p->fe.consistent;
     r->seed_used = p->seed_used;
+    r->singular_complete = (p->opt.flags & BDEG_FLAG_DEGREE_ONLY) ? 0 : 1;
     r->relifts = p->relifts;
     r->total_candidates = p->total;
     r->plan_ms = p->plan_ms;
@@ -361,6 +363,7 @@ bdeg_status slots_to_result(bdeg_plan_s *p, const int64_t *h, bdeg_result *r) {
     r->overflow_reruns = (uint64_t)h[SLOT_OVF_BLOCKS];
     r->updates = (uint64_t)h[SLOT_UPDATES];
     r->leaves = (uint64_t)h[SLOT_LEAVES];
+    r->dead_leaves = (uint64_t)h[SLOT_DEAD];
     return BDEG_OK;
 }
 

@@ -74,6 +74,7 @@ struct LaunchArgs {
     int bits_v, bits_l;               // tier-1 bounds: |V| < 2^bits_v, |lift| < 2^bits_l
     int replay;                       // 1: process ovf_queue[0..*ovf_count) in tier 2
     int grid, block;                  // launch shape
+    int degree_only;                  // skip cell-dead subtrees
     void *stream;
 };
 
@@ -84,7 +85,8 @@ enum Slot {
     SLOT_OVF_BLOCKS = 8,   // int32-tier blocks queued for re-run
     SLOT_FATAL = 9,        // int64-tier overflow (value beyond int64)
     SLOT_QFULL = 10,       // overflow queue exhausted
-    SLOT_BLOCKS = 11, SLOT_UPDATES = 12, SLOT_LEAVES = 13
+    SLOT_BLOCKS = 11, SLOT_UPDATES = 12, SLOT_LEAVES = 13,
+    SLOT_DEAD = 14         // leaves inside cell-dead subtrees (singular count only)
 };
 
 // Dynamic shared memory bytes for a launch of the enumeration kernel.

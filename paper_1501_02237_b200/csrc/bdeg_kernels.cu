@@ -161,8 +161,8 @@ __device__ __forceinline__ float unford(uint32_t o) {   // inverse of ford
 // Per-item accumulators (warp-uniform: every lane holds the same values).
 struct Acc {
     uint64_t vol_lo, vol_hi, singular, cand, updates;
-    uint32_t cells, ties, leaves;
-    __device__ void zero() { vol_lo = vol_hi = singular = cand = updates = 0; cells = ties = leaves = 0; }
+    uint32_t cells, ties, leaves, dead;
+    __device__ void zero() { vol_lo = vol_hi = singular = cand = updates = 0; cells = ties = leaves = dead = 0; }
     __device__ void add_vol(uint64_t v) {
         uint64_t t = vol_lo + v;
         vol_hi += (t < vol_lo);
@@ -171,14 +171,14 @@ struct Acc {
 };
 // Per-warp totals.
 struct WAcc {
-    uint64_t vol_lo, vol_hi, cells, singular, cand, ties, updates, leaves;
-    __device__ void zero() { vol_lo = vol_hi = cells = singular = cand = ties = updates = leaves = 0; }
+    uint64_t vol_lo, vol_hi, cells, singular, cand, ties, updates, leaves, dead;
+    __device__ void zero() { vol_lo = vol_hi = cells = singular = cand = ties = updates = leaves = dead = 0; }
     __device__ void add(const Acc &o) {
         uint64_t t = vol_lo + o.vol_lo;
         vol_hi += (t < vol_lo) + o.vol_hi;
         vol_lo = t;
         cells += o.cells; singular += o.singular; cand += o.cand; ties += o.ties;
-        updates += o.updates; leaves += o.leaves;
+        updates += o.updates; leaves += o.leaves; dead += o.dead;
     }
 };
 
@@ -191,6 +191,7 @@ struct Ctx {
     int D, kd, fmin;     // item depth, K - D, smallest forced DFS level
     int mytop;           // this lane's entry of the item tuple: c_{kd + lane} (lane < D)
     uint64_t irb, ire;   // the item's candidates n [rb, re)
+    bool deg_only;       // skip cell-dead subtrees (singular count becomes a lower bound)
     bool partial;
     __device__ __forceinline__ uint64_t C(int n, int k) const { return B[n * kBinomCols + k]; }
     // |[base, base+size) n [rb, re)|
@@ -356,11 +357,35 @@ __device__ __forceinline__ void fetch_col(const typename Tr<TIER>::VV (&sv)[NPL]
 // no division is needed, since slopes and cross-product signs are invariant
 // under the common factor prev, whose sign is folded into kappa'
 // (= sign(piv) * sign(prev)).  |det| = |X_j| / |prev| for the (rare) cells.
+// Cell-dead test of a DFS node (P:913-929 monotonicity, in determinant
+// form).  If a point l outside the prefix has all remaining V-row values 0
+// (v_l lies in the span of the prefix vectors), its lift residual y_l only
+// gets multiplied by pivot ratios further down: at any leaf of this subtree
+// the facet test reads sign(g) * y_l with g the node's last pivot.  A
+// negative value means l lies strictly below every hyperplane through the
+// prefix: no cell exists in the subtree (only the singular count remains).
+template <int TIER, int NPL, int RV>
+__device__ __forceinline__ bool node_dead(const typename Tr<TIER>::VV (&sv)[NPL][RV],
+                                          const typename Tr<TIER>::VL (&sl)[NPL], uint64_t inP,
+                                          int64_t g, const Ctx &cx) {
+    bool below = false;
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) {
+        const int l = cx.lane + 32 * q;
+        bool zero = true;
+#pragma unroll
+        for (int r = 0; r < RV; ++r) zero &= sv[q][r] == 0;
+        const bool neg = (g > 0) ? (sl[q] < 0) : (sl[q] > 0);
+        below |= zero && neg && l < cx.N && !((inP >> l) & 1ull);
+    }
+    return __any_sync(FULL, below);
+}
+
 template <int TIER, int NPL>
 __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL][2],
                                            const typename Tr<TIER>::VL (&sl)[NPL], int lo, int hi,
                                            uint64_t base, uint64_t inP, int64_t prev, const Ctx &cx,
-                                           Acc &acc) {
+                                           Acc &acc, bool dead) {
     typedef typename Tr<TIER>::VV VV;
     typedef typename Tr<TIER>::VL VL;
     const uint64_t gabs = (uint64_t)(prev < 0 ? -prev : prev);
@@ -403,6 +428,20 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
         const bool p0 = u != 0;
         const VV piv = p0 ? u : v;
         const VV ncs = p0 ? -v : -u;               // -(pivot column entry of the other row)
+        if (dead) {                                // no cell below: singular count only
+            unsigned sd = 0;
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int l = cx.lane + 32 * q;
+                const VV prow = p0 ? sv[q][0] : sv[q][1];
+                const VV s = p0 ? sv[q][1] : sv[q][0];
+                const int64_t x = madw(piv, s, mulw(ncs, prow));
+                sd += __popc(__ballot_sync(FULL, l >= jlo && l < jhi && x == 0));
+            }
+            acc.singular += sd;
+            acc.dead += 1;
+            continue;
+        }
         const bool kneg = (piv < 0) != gneg;
         const VV pz = kneg ? (VV)-piv : piv;
         const VL ncz = kneg ? z : (VL)-z;
@@ -484,7 +523,7 @@ template <int TIER, int NPL, int RV>
 __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL][RV],
                                           const typename Tr<TIER>::VL (&sl)[NPL], int cbound,
                                           uint64_t base, uint64_t inP, int64_t prev, const Ctx &cx,
-                                          Acc &acc, bool &ovf) {
+                                          Acc &acc, bool &ovf, bool dead) {
     typedef typename Tr<TIER>::VV VV;
     typedef typename Tr<TIER>::VL VL;
     constexpr int i = RV - 1;
@@ -494,7 +533,7 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
         hi = lo + 1;
     }
     if constexpr (RV == 2 && TIER != 2) {
-        leaf_level<TIER, NPL>(sv, sl, lo, hi, base, inP, prev, cx, acc);
+        leaf_level<TIER, NPL>(sv, sl, lo, hi, base, inP, prev, cx, acc, dead);
         return;
     }
     Div dv;
@@ -540,7 +579,13 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
             // overflow is voted once per item (the item is discarded and replayed);
             // loops are index-bounded, so garbage values cannot hang the warp
             elim_step<TIER, NPL, RV>(sv, sl, cv, cl, pr, piv, dv, cx, ov, ol, ovf);
-            inner_dfs<TIER, NPL, RV - 1>(ov, ol, c, nb, inP | (1ull << c), (int64_t)piv, cx, acc, ovf);
+            const uint64_t cinP = inP | (1ull << c);
+            const bool cdead = dead || node_dead<TIER, NPL, RV - 1>(ov, ol, cinP, (int64_t)piv, cx);
+            if (cdead && cx.deg_only) {          // no cell in the subtree: skip it
+                acc.cand += (i >= cx.fmin) ? cx.ire - cx.irb : cx.isect(nb, ns);
+                continue;
+            }
+            inner_dfs<TIER, NPL, RV - 1>(ov, ol, c, nb, cinP, (int64_t)piv, cx, acc, ovf, cdead);
         }
     }
 }
@@ -699,7 +744,12 @@ __device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, co
         for (int q = 0; q < NPL; ++q) { xx[q] = (int64_t)sv[q][0]; yy[q] = (int64_t)sl[q]; }
         leaf_test<NPL>(xx, yy, ctop, ttop, inP, prev > 0 ? 1 : -1, 1, cx, acc);
     } else {
-        inner_dfs<TIER, NPL, S + 1>(sv, sl, ctop, ttop, inP, prev, cx, acc, ovf);
+        const bool dead = node_dead<TIER, NPL, S + 1>(sv, sl, inP, prev, cx);
+        if (dead && cx.deg_only) {
+            acc.cand += cx.ire - cx.irb;
+            return;
+        }
+        inner_dfs<TIER, NPL, S + 1>(sv, sl, ctop, ttop, inP, prev, cx, acc, ovf, dead);
     }
 }
 
@@ -773,6 +823,7 @@ k_enumerate(LaunchArgs a) {
     int64_t *scr = scr_all + (size_t)warp * (K + 1) * 32 * NPL;
 
     cx.D = a.P.D;
+    cx.deg_only = a.degree_only != 0;
     cx.kd = K - a.P.D;
     cx.fmin = (a.P.D > T) ? K - a.P.D : S + 1;
     cx.mytop = 0;
@@ -827,7 +878,7 @@ k_enumerate(LaunchArgs a) {
         w[SLOT_BLOCKS] = n_blocks;
         w[SLOT_UPDATES] = wacc.updates;
         w[SLOT_LEAVES] = wacc.leaves;
-        w[14] = 0;
+        w[14] = wacc.dead;
         w[15] = 0;
     }
     __syncthreads();

@@ -238,3 +238,22 @@ def test_w34_w26_full():
     for mk, want in [((3, 4), 26762), ((2, 6), 22304)]:
         A, b = W.master_space_system(*mk)
         assert B.degree(A, b, seed=1).degree == want
+
+
+@pytest.mark.parametrize("name", ["W2_3", "W3_2", "dp0", "rnc7"])
+def test_degree_only_mode(name):
+    # skipping cell-dead subtrees (P:913-929 monotonicity) keeps degree, cells,
+    # candidates and ties exact; the singular count becomes a lower bound
+    A, b = W.named_system(name)
+    lift = W.liftings(len(A) + 1, 1)
+    full = B.Plan.from_system(A, b, lift).degree()
+    fast = B.Plan.from_system(A, b, lift, flags=0x40).degree()
+    assert (fast.degree, fast.cells, fast.candidates, fast.ties) == (full.degree, full.cells, full.candidates, full.ties)
+    assert fast.singular <= full.singular and not fast.singular_complete and full.singular_complete
+
+
+def test_degree_only_table3(table3):
+    for mk in [(2, 4), (3, 3), (2, 5)]:
+        A, b = W.master_space_system(*mk)
+        r = B.degree(A, b, seed=1, flags=0x40)
+        assert r.degree == table3[mk][0] and r.candidates == r.total_candidates

@@ -21,7 +21,7 @@ for wl in wls:
     for S in Ss:
         if S > K - 1:
             continue
-        p = B.Plan.from_points(V, w, inner_levels=S)
+        p = B.Plan.from_points(V, w, inner_levels=S, flags=int(os.environ.get("SWEEP_FLAGS", "0"), 0))
         r = p.degree()   # warm
         reps = 3 if total < 1e10 else 1
         t0 = time.perf_counter()
@@ -29,5 +29,5 @@ for wl in wls:
             r = p.degree()
         dt = (time.perf_counter() - t0) / reps
         print(json.dumps({"wl": wl, "S": S, "tier": r.tier, "ms": dt * 1e3, "kernel_ms": r.kernel_ms,
-                          "rate": total / dt, "degree": r.degree, "leaves": r.leaves}), flush=True)
+                          "rate": total / dt, "degree": r.degree, "leaves": r.leaves, "dead": r.dead_leaves}), flush=True)
         p.close()
