@@ -45,8 +45,9 @@ def workload(name):
         V, w = W.c5_points(1)
         return ("C5 synthetic: K=8 vectors (1,a), a uniform in [-3,3]^7, N=40 distinct points, "
                 "lifting uniform in [0,2^20) (SplitMix64 seed 1)", 8, V, w, {"seed": 1})
-    m, k = {"w24": (2, 4), "w33": (3, 3), "w25": (2, 5), "w26": (2, 6), "w34": (3, 4),
-            "w27": (2, 7)}[name]
+    if not (name.startswith("w") and len(name) == 3 and name[1:].isdigit()):
+        raise SystemExit(f"unknown workload {name!r} (c5 or w<m><k>)")
+    m, k = int(name[1]), int(name[2])
     from oracle import point_configuration  # input preparation only (front end of the oracle)
     A, b = W.master_space_system(m, k)
     lift = W.liftings(len(A) + 1, 1)
