@@ -80,7 +80,7 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:  # noqa: BLE001
             self.proc = None
@@ -204,6 +204,7 @@ def run_gpu(args):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        time.sleep(0.3)                                  # let nvidia-smi attach before timing
         t_wall0 = time.perf_counter()
         for s in range(args.steps):
             flush.fill_(float(s))                       # L2 flush (outside the events)
@@ -214,6 +215,7 @@ def run_gpu(args):
         t_wall = time.perf_counter() - t_wall0
         if world > 1:
             dist.barrier()
+        time.sleep(0.05)
     launches = B.launch_count() - launches0
     ms = [a.elapsed_time(b) for a, b in evs]
     ms_step = statistics.mean(ms)
@@ -228,7 +230,8 @@ def run_gpu(args):
     e2e_ms = []
     h2d = (((K + 1) * len(V) * 8 + 15) // 16) * 16 + 65 * 34 * 8
     d2h = B.NSLOTS * 8
-    for s in range(args.warmup + args.steps):
+    e2e_steps = min(args.steps, 30)     # a plan per step: bounded to keep the run short
+    for s in range(args.warmup + e2e_steps):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -303,7 +306,7 @@ def run_gpu(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="bdeg", choices=["bdeg", "reference"])
     ap.add_argument("--workload", default="c5")

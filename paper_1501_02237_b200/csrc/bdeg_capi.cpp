@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -133,7 +134,7 @@ void sample_bits(const bdeg_plan_s *p, int &bv, int &bl) {
     SplitMix64 g(0x5eed ^ p->seed_used);
     i128 mv = 1, ml = 1;
     bool big = false;
-    for (int s = 0; s < 128 && !big; ++s) {
+    for (int s = 0; s < 32 && !big; ++s) {
         std::vector<int> perm(N);
         for (int i = 0; i < N; ++i) perm[i] = i;
         for (int i = N - 1; i > 0; --i) std::swap(perm[i], perm[g.next() % (uint64_t)(i + 1)]);
@@ -230,6 +231,52 @@ void rebuild_points(bdeg_plan_s *p) {
                  p->w, p->point_of_var, p->origin_index);
 }
 
+// Per-device properties (queried once per process) and a small pool of
+// device workspaces, so that planning a new problem does not pay
+// cudaGetDeviceProperties / cudaMalloc / cudaFree every time.
+struct DevInfo { bool ok = false; int sms = 0, major = 0; };
+std::mutex g_mu;
+DevInfo g_dev[64];
+std::vector<std::pair<size_t, void *>> g_pool[64];
+
+const DevInfo &dev_info(int d) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_dev[d].ok) {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, d) == cudaSuccess) {
+            g_dev[d].sms = prop.multiProcessorCount;
+            g_dev[d].major = prop.major;
+            g_dev[d].ok = true;
+        }
+    }
+    return g_dev[d];
+}
+
+void *pool_get(int d, size_t bytes, size_t *got) {
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto &v = g_pool[d];
+        for (size_t i = 0; i < v.size(); ++i)
+            if (v[i].first >= bytes) {
+                void *ptr = v[i].second;
+                *got = v[i].first;
+                v.erase(v.begin() + i);
+                return ptr;
+            }
+    }
+    void *ptr = nullptr;
+    if (cudaMalloc(&ptr, bytes) != cudaSuccess) return nullptr;
+    *got = bytes;
+    return ptr;
+}
+
+void pool_put(int d, void *ptr, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto &v = g_pool[d];
+    if (v.size() < 8) v.push_back({bytes, ptr});
+    else cudaFree(ptr);
+}
+
 bdeg_status ensure_device(bdeg_plan_s *p) {
     cudaError_t e;
     if (!p->dev_ready) {
@@ -237,14 +284,16 @@ bdeg_status ensure_device(bdeg_plan_s *p) {
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= p->opt.device)
             return fail(p, BDEG_E_CUDA, "no CUDA device available (libbdeg has no CPU fallback)");
         if ((e = cudaSetDevice(p->opt.device)) != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
-        cudaDeviceProp prop;
-        cudaGetDeviceProperties(&prop, p->opt.device);
-        if (prop.major < 10) return fail(p, BDEG_E_CUDA, "libbdeg is built for sm_100a (B200); device is older");
+        const DevInfo &di = dev_info(p->opt.device);
+        if (!di.ok) return fail(p, BDEG_E_CUDA, "cudaGetDeviceProperties failed");
+        if (di.major < 10) return fail(p, BDEG_E_CUDA, "libbdeg is built for sm_100a (B200); device is older");
         const Layout L = layout(p);
         if (!p->ws) {
-            if ((e = cudaMalloc(&p->ws, L.total)) != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
+            size_t got = 0;
+            p->ws = (char *)pool_get(p->opt.device, L.total, &got);
+            if (!p->ws) return fail(p, BDEG_E_CUDA, "cudaMalloc of the workspace failed");
             p->own_ws = true;
-            p->ws_bytes = L.total;
+            p->ws_bytes = got;
         } else if (p->ws_bytes < L.total) {
             return fail(p, BDEG_E_INVALID, "workspace too small");
         }
@@ -264,7 +313,7 @@ bdeg_status ensure_device(bdeg_plan_s *p) {
         a.tier = p->tier;
         const int occ = std::max(enumerate_max_ctas_per_sm(a), 1);
         const int per_sm = p->opt.ctas_per_sm > 0 ? std::min(p->opt.ctas_per_sm, occ) : occ;
-        p->grid = prop.multiProcessorCount * per_sm;
+        p->grid = di.sms * per_sm;
         p->dev_ready = true;
     }
     if (p->l_dirty) {
@@ -640,7 +689,7 @@ const char *bdeg_status_str(bdeg_status s) {
 
 void bdeg_destroy(bdeg_plan_t p) {
     if (!p) return;
-    if (p->own_ws && p->ws) cudaFree(p->ws);
+    if (p->own_ws && p->ws) pool_put(p->opt.device, p->ws, p->ws_bytes);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
     delete p;

@@ -27,6 +27,8 @@
 
 #include <cuda_runtime.h>
 #include <atomic>
+#include <map>
+#include <mutex>
 
 namespace bdeg {
 
@@ -915,12 +917,26 @@ static KernFn pick(int tier, int npl, int S) {
     return nullptr;
 }
 
+// cudaFuncSetAttribute(max dynamic smem) once per (kernel, size): the value
+// only ever grows, so remember the largest one set per kernel
+static std::mutex g_attr_mu;
+static std::map<KernFn, size_t> g_attr;
+
+static cudaError_t ensure_smem_attr(KernFn f, size_t smem) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = g_attr.find(f);
+    if (it != g_attr.end() && it->second >= smem) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) g_attr[f] = smem;
+    return e;
+}
+
 int enumerate_max_ctas_per_sm(const LaunchArgs &a) {
     const int npl = a.P.N > 32 ? 2 : 1;
     KernFn f = pick(a.tier, npl, a.P.S);
     if (!f) return 1;
     const size_t smem = enumerate_smem_bytes(a.P.K, a.P.N, dev::kWarps);
-    cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem_attr(f, smem);
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, dev::kWarps * 32, smem) != cudaSuccess) return 1;
     return n > 0 ? n : 1;
@@ -931,7 +947,7 @@ int launch_enumerate(const LaunchArgs &a) {
     KernFn f = pick(a.tier, npl, a.P.S);
     if (!f) return (int)cudaErrorInvalidValue;
     const size_t smem = enumerate_smem_bytes(a.P.K, a.P.N, dev::kWarps);
-    cudaError_t e = cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_smem_attr(f, smem);
     if (e != cudaSuccess) return (int)e;
     f<<<a.grid, dev::kWarps * 32, smem, (cudaStream_t)a.stream>>>(a);
     launch_counter_add(1);
