@@ -168,6 +168,23 @@ bdeg_status bdeg_item_range(bdeg_plan_t plan, uint64_t item, uint64_t *begin, ui
  * the stream.  Combine with one all-reduce(SUM) and call bdeg_finalize. */
 bdeg_status bdeg_degree_partial(bdeg_plan_t plan, int64_t *d_slots);
 
+/* cell emission: the cells of the subdivision among the colex
+ * ranks [begin, end), as (mask, |det|) pairs into h_out (HOST, 2*capacity
+ * uint64): bit l of mask = point l (bdeg_plan_info's point order).  *count =
+ * cells found (may exceed capacity; only capacity pairs are written). */
+bdeg_status bdeg_cells(bdeg_plan_t plan, uint64_t begin, uint64_t end, uint64_t *h_out, uint64_t capacity,
+                       uint64_t *count);
+
+/* output-sensitive degree: walk the regular subdivision cell to
+ * cell across ridges (the paper's pivoting, and its graph view,
+ * P:1068-1132), each pivot an exact warp-wide ridge test, cells deduplicated
+ * in a device hash set, volumes summed exactly.  Work ~ cells x K
+ * instead of C(N,K).  Result: degree and cells exact (same subdivision as
+ * bdeg_degree for the same lifting); candidates/singular are not enumerated
+ * (singular_complete = 0); leaves = ridge tests, dead_leaves = boundary ridges.
+ * Re-lifts generated liftings on ties like bdeg_degree. */
+bdeg_status bdeg_degree_walk(bdeg_plan_t plan, bdeg_result *out);
+
 /* Carry-normalise summed slots (HOST memory) into *out. */
 bdeg_status bdeg_finalize(bdeg_plan_t plan, const int64_t *h_slots, bdeg_result *out);
 

@@ -27,6 +27,6 @@ from .snf import smith_normal_form, det_fraction, rank_fraction  # noqa: F401
 from .binomial import analyze  # noqa: F401
 from .points import point_configuration  # noqa: F401
 from .subdivision import (  # noqa: F401
-    binom, colex_rank, colex_unrank, enumerate_lifted, degree,
+    binom, colex_rank, colex_unrank, enumerate_lifted, degree, cell_list,
 )
 from .volume import nvol_pulling  # noqa: F401

@@ -177,6 +177,26 @@ def enumerate_lifted(K, objs, lifts, rank_begin=0, rank_end=None, test="cone"):
     return res
 
 
+def cell_list(K, objs, lifts, rank_begin=0, rank_end=None, test="cone"):
+    """The cells themselves (index tuples with their NVol) among the ranks
+    [rank_begin, rank_end) — the simplicial subdivision D of Def. 1."""
+    N = len(objs)
+    total = binom(N, K)
+    if rank_end is None or rank_end > total:
+        rank_end = total
+    fn = lower_face_cone if test == "cone" else lower_face_affine
+    out = []
+    if rank_begin >= rank_end:
+        return out
+    c = colex_unrank(rank_begin, K)
+    for _ in range(rank_end - rank_begin):
+        status, nvol = fn(objs, lifts, c)
+        if status == "cell":
+            out.append((tuple(c), nvol))
+        c = colex_next(c, N)
+    return sorted(out)
+
+
 def degree(A, b=None, lifting=None, test="cone", rank_begin=0, rank_end=None):
     """deg V of each component of V*(x^A - b) (Prop. 4) by the
     lifted brute force.  Returns dict(dim, components, degree, cells,

@@ -83,7 +83,7 @@ EXPORTS = ["bdeg_default_options", "bdeg_plan", "bdeg_plan_points", "bdeg_plan_i
            "bdeg_workspace_bytes", "bdeg_set_workspace", "bdeg_degree", "bdeg_degree_range",
            "bdeg_degree_partial", "bdeg_finalize", "bdeg_relift", "bdeg_last_error",
            "bdeg_status_str", "bdeg_destroy", "bdeg_launch_count", "bdeg_num_items",
-           "bdeg_item_range"]
+           "bdeg_item_range", "bdeg_cells", "bdeg_degree_walk"]
 
 
 def _load():
@@ -117,6 +117,11 @@ def _load():
     lib.bdeg_num_items.restype = ctypes.c_uint64
     lib.bdeg_item_range.argtypes = [plan_t, ctypes.c_uint64, P(ctypes.c_uint64), P(ctypes.c_uint64)]
     lib.bdeg_item_range.restype = ctypes.c_int
+    lib.bdeg_cells.argtypes = [plan_t, ctypes.c_uint64, ctypes.c_uint64, P(ctypes.c_uint64),
+                               ctypes.c_uint64, P(ctypes.c_uint64)]
+    lib.bdeg_cells.restype = ctypes.c_int
+    lib.bdeg_degree_walk.argtypes = [plan_t, P(_Result)]
+    lib.bdeg_degree_walk.restype = ctypes.c_int
     lib.bdeg_launch_count.argtypes = []
     lib.bdeg_launch_count.restype = ctypes.c_uint64
     for name in ["bdeg_plan", "bdeg_plan_points", "bdeg_plan_info", "bdeg_set_workspace",
@@ -308,6 +313,27 @@ class Plan:
         r = _Result()
         _check(lib.bdeg_degree(self._h, ctypes.byref(r)), self._h)
         return _result(r)
+
+    def degree_walk(self) -> Result:
+        """Output-sensitive degree by walking the subdivision."""
+        r = _Result()
+        _check(lib.bdeg_degree_walk(self._h, ctypes.byref(r)), self._h)
+        return _result(r)
+
+    def cells(self, begin: int = 0, end: int = None, capacity: int = 1 << 20):
+        """Cells among ranks [begin, end) as a list of (point-index tuple, |det|)."""
+        if end is None:
+            end = self.info().total_candidates
+        buf = (ctypes.c_uint64 * (2 * max(1, capacity)))()
+        n = ctypes.c_uint64()
+        _check(lib.bdeg_cells(self._h, begin, end, buf, capacity, ctypes.byref(n)), self._h)
+        if n.value > capacity:
+            raise BdegError(BDEG_E_TOO_LARGE, f"{n.value} cells exceed capacity {capacity}")
+        out = []
+        for i in range(n.value):
+            m, v = buf[2 * i], buf[2 * i + 1]
+            out.append((tuple(l for l in range(64) if (m >> l) & 1), v))
+        return sorted(out)
 
     def degree_range(self, begin: int, end: int) -> Result:
         r = _Result()

@@ -337,7 +337,8 @@ bdeg_status ensure_device(bdeg_plan_s *p) {
 // Enqueue the enumeration of ranks [b, e) (this rank's interleaved share of
 // blocks) accumulating into `slots` (zeroed here).
 bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long long *slots, int rank,
-                          int world, int force_tier) {
+                          int world, int force_tier, unsigned long long *cells_out = nullptr,
+                          unsigned long long *cells_cnt = nullptr, uint64_t cells_cap = 0) {
     cudaStream_t st = (cudaStream_t)p->opt.stream;
     cudaError_t ce;
     if ((ce = cudaMemsetAsync(slots, 0, kNSlots * 8, st)) != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
@@ -363,6 +364,9 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     a.tier = force_tier >= 0 ? force_tier : p->tier;
     a.bits_v = p->bits_v;
     a.degree_only = (p->opt.flags & BDEG_FLAG_DEGREE_ONLY) ? 1 : 0;
+    a.cells_out = cells_out;
+    a.cells_cnt = cells_cnt;
+    a.cells_cap = cells_cap;
     a.bits_l = p->bits_l;
     a.replay = 0;
     a.counter = p->d_ctr + 0;
@@ -435,6 +439,135 @@ bdeg_status run_sync(bdeg_plan_s *p, uint64_t b, uint64_t e, int64_t *h, double 
         *kms += ms;
         if (h[SLOT_QFULL] == 0) return BDEG_OK;
     }
+    return BDEG_OK;
+}
+
+// Device buffers of one walk (freed on scope exit).
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+    bool alloc(size_t bytes) {
+        if (p) { cudaFree(p); p = nullptr; }
+        return cudaMalloc(&p, bytes) == cudaSuccess;
+    }
+    unsigned long long *u() const { return (unsigned long long *)p; }
+};
+
+// Cells (mask, |det|) of ranks [b, e) into host memory (tier 2: no replays,
+// so nothing is emitted twice).
+bdeg_status cells_range(bdeg_plan_s *p, uint64_t b, uint64_t e, uint64_t *h_out, uint64_t cap, uint64_t *count) {
+    bdeg_status s = ensure_device(p);
+    if (s) return s;
+    cudaStream_t st = (cudaStream_t)p->opt.stream;
+    DevBuf buf, cnt;
+    if (!buf.alloc((2 * std::max<uint64_t>(cap, 1)) * 8) || !cnt.alloc(8))
+        return fail(p, BDEG_E_CUDA, "cudaMalloc failed");
+    cudaMemsetAsync(cnt.p, 0, 8, st);
+    s = enqueue_range(p, b, e, p->d_slots, 0, 1, 2, buf.u(), cnt.u(), cap);
+    if (s) return s;
+    uint64_t n = 0;
+    cudaMemcpyAsync(&n, cnt.p, 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+    const uint64_t m = std::min(n, cap);
+    if (m && h_out) {
+        ce = cudaMemcpy(h_out, buf.p, m * 16, cudaMemcpyDeviceToHost);
+        if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+    }
+    *count = n;
+    return BDEG_OK;
+}
+
+uint64_t pow2_at_least(uint64_t x) {
+    uint64_t c = 1;
+    while (c < x) c <<= 1;
+    return c;
+}
+
+// One breadth-first walk of the subdivision.
+bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
+    cudaStream_t st = (cudaStream_t)p->opt.stream;
+    const double t0 = now_ms();
+    // 1. a starting cell from the enumeration kernel over a growing rank prefix
+    uint64_t start = 0;
+    {
+        uint64_t pair[2 * 16];
+        for (uint64_t L = 1ull << 16;; L *= 8) {
+            uint64_t n = 0;
+            bdeg_status s = cells_range(p, 0, std::min(L, p->total), pair, 16, &n);
+            if (s) return s;
+            if (n > 0) { start = pair[0]; break; }
+            if (L >= p->total) return fail(p, BDEG_E_DEGENERATE, "no cell found (degenerate lifting)");
+        }
+    }
+    // 2. the walk
+    const int K = p->K;
+    uint64_t cap = 1ull << 20, ncur = 1, total_cells = 1;
+    DevBuf table, cur, nxt, aux;
+    if (!table.alloc(cap * 8) || !cur.alloc(cap * 8) || !nxt.alloc(cap * 8) || !aux.alloc(16 * 8))
+        return fail(p, BDEG_E_CUDA, "cudaMalloc failed");
+    unsigned long long *next_cnt = aux.u(), *counter = aux.u() + 1, *stats = aux.u() + 2;   // stats: 8 slots
+    cudaMemsetAsync(table.p, 0, cap * 8, st);
+    const uint64_t h0 = walk_hash(start) & (cap - 1);
+    cudaMemcpyAsync(table.u() + h0, &start, 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(cur.p, &start, 8, cudaMemcpyHostToDevice, st);
+    const int grid = std::max(1, dev_info(p->opt.device).sms) * 4;
+    uint64_t ridges = 0, boundary = 0;
+    while (ncur > 0) {
+        if ((total_cells + ncur * K) * 2 > cap) {               // grow: rehash + bigger frontiers
+            const uint64_t ncap = pow2_at_least(4 * (total_cells + ncur * K));
+            DevBuf t2, c2;
+            if (!t2.alloc(ncap * 8) || !c2.alloc(ncap * 8)) return fail(p, BDEG_E_CUDA, "cudaMalloc (grow) failed");
+            cudaMemsetAsync(t2.p, 0, ncap * 8, st);
+            cudaMemsetAsync(stats, 0, 8 * 8, st);
+            int rc = launch_rehash(table.u(), cap, t2.u(), ncap, stats + 3, st);
+            if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
+            cudaMemcpyAsync(c2.p, cur.p, ncur * 8, cudaMemcpyDeviceToDevice, st);
+            cudaStreamSynchronize(st);
+            std::swap(table.p, t2.p);
+            std::swap(cur.p, c2.p);
+            if (!nxt.alloc(ncap * 8)) return fail(p, BDEG_E_CUDA, "cudaMalloc (grow) failed");
+            cap = ncap;
+        }
+        cudaMemsetAsync(aux.p, 0, 16 * 8, st);
+        int rc = launch_walk(p->d_L, K, p->N, cur.u(), ncur, nxt.u(), next_cnt, table.u(), cap, counter, stats,
+                             grid, st);
+        if (rc) return fail(p, BDEG_E_CUDA, std::string("k_walk: ") + cudaGetErrorString((cudaError_t)rc));
+        uint64_t h[10];
+        cudaMemcpyAsync(h, aux.p, 10 * 8, cudaMemcpyDeviceToHost, st);
+        cudaError_t ce = cudaStreamSynchronize(st);
+        if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+        const uint64_t *sv = h + 2;
+        ridges += sv[0];
+        boundary += sv[5];
+        if (sv[1] > 0) return fail(p, BDEG_E_DEGENERATE, "degenerate lifting: a ridge has a tie (cell walk)");
+        if (sv[2] > 0 || sv[4] > 0 || sv[3] > 0)
+            return fail(p, BDEG_E_TOO_LARGE, "cell walk: inconsistent ridge, value overflow or full table");
+        std::swap(cur.p, nxt.p);
+        ncur = h[0];
+        total_cells += ncur;
+    }
+    // 3. exact volumes, one determinant per cell
+    cudaMemsetAsync(aux.p, 0, 16 * 8, st);
+    int rc = launch_cellvol(p->d_L, K, p->N, table.u(), cap, aux.u() + 8, aux.u(), grid, st);
+    if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
+    uint64_t h[16];
+    cudaMemcpyAsync(h, aux.p, 16 * 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+    if (h[8 + 5] > 0) return fail(p, BDEG_E_TOO_LARGE, "cell volume overflow");
+    u128 vol = 0;
+    for (int i = 3; i >= 0; --i) vol = (vol << 32) + (u128)h[8 + i];
+    r->deg_lo = (uint64_t)vol;
+    r->deg_hi = (int64_t)(uint64_t)(vol >> 64);
+    r->cells = h[8 + 4];
+    r->candidates = 0;
+    r->singular = 0;
+    r->singular_complete = 0;
+    r->leaves = ridges;          // ridge tests (pivots)
+    r->dead_leaves = boundary;   // boundary ridges
+    if (r->cells != total_cells) return fail(p, BDEG_E_TOO_LARGE, "cell walk: table / frontier mismatch");
+    *kms += now_ms() - t0;
     return BDEG_OK;
 }
 
@@ -668,6 +801,46 @@ bdeg_status bdeg_item_range(bdeg_plan_t p, uint64_t item, uint64_t *begin, uint6
     }
     *begin = base;
     *end = base + C(p->binom, first, kd);
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_cells(bdeg_plan_t p, uint64_t begin, uint64_t end, uint64_t *h_out, uint64_t capacity,
+                       uint64_t *count) {
+    if (!p || !count) return fail(p, BDEG_E_INVALID, "NULL argument");
+    *count = 0;
+    if (p->K == 0) return BDEG_OK;
+    return cells_range(p, begin, end, h_out, capacity, count);
+}
+
+bdeg_status bdeg_degree_walk(bdeg_plan_t p, bdeg_result *out) {
+    if (!p || !out) return fail(p, BDEG_E_INVALID, "NULL argument");
+    const double t0 = now_ms();
+    bdeg_result r;
+    fill_front(p, &r);
+    if (p->K == 0) {
+        r.deg_lo = 1;
+        *out = r;
+        return BDEG_OK;
+    }
+    bdeg_status s = ensure_device(p);
+    if (s) return s;
+    double kms = 0;
+    for (int attempt = p->relifts;; ++attempt) {
+        fill_front(p, &r);
+        s = walk_once(p, &r, &kms);
+        if (s != BDEG_E_DEGENERATE) break;
+        if (p->user_lift || (p->opt.flags & BDEG_FLAG_NO_RELIFT)) return s;
+        if (attempt + 1 > p->opt.max_relift) return s;
+        bdeg_relift(p, attempt + 1);
+        s = ensure_device(p);
+        if (s) return s;
+    }
+    if (s) return s;
+    r.relifts = p->relifts;
+    r.seed_used = p->seed_used;
+    r.kernel_ms = kms;
+    r.total_ms = now_ms() - t0;
+    *out = r;
     return BDEG_OK;
 }
 

@@ -75,6 +75,9 @@ struct LaunchArgs {
     int replay;                       // 1: process ovf_queue[0..*ovf_count) in tier 2
     int grid, block;                  // launch shape
     int degree_only;                  // skip cell-dead subtrees
+    unsigned long long *cells_out;    // optional (mask, |det|) output of the cells found
+    unsigned long long *cells_cnt;
+    uint64_t cells_cap;
     void *stream;
 };
 
@@ -98,5 +101,16 @@ int kernel_warps_per_cta();
 int enumerate_max_ctas_per_sm(const LaunchArgs &a);
 
 uint64_t launch_counter_add(uint64_t k);
+
+// ---- cell walk, bdeg_walk.cu
+size_t walk_smem_bytes(int K, int N);
+uint64_t walk_hash(uint64_t key);
+int launch_walk(const int64_t *L, int K, int N, const unsigned long long *cur, uint64_t ncur,
+                unsigned long long *next, unsigned long long *next_cnt, unsigned long long *table, uint64_t cap,
+                unsigned long long *counter, unsigned long long *stats, int grid, void *stream);
+int launch_cellvol(const int64_t *L, int K, int N, const unsigned long long *table, uint64_t cap,
+                   unsigned long long *out, unsigned long long *counter, int grid, void *stream);
+int launch_rehash(const unsigned long long *old, uint64_t oldcap, unsigned long long *tab, uint64_t cap,
+                  unsigned long long *full_flag, void *stream);
 
 }  // namespace bdeg

@@ -195,6 +195,18 @@ struct Ctx {
     uint64_t irb, ire;   // the item's candidates n [rb, re)
     bool deg_only;       // skip cell-dead subtrees (singular count becomes a lower bound)
     bool partial;
+    unsigned long long *cells_out;   // optional (mask, |det|) pairs of the cells found
+    unsigned long long *cells_cnt;
+    uint64_t cells_cap;
+    __device__ __forceinline__ void emit(uint64_t mask, uint64_t vol) const {
+        if (cells_out && lane == 0) {
+            const unsigned long long pos = atomicAdd(cells_cnt, 1ull);
+            if (pos < cells_cap) {
+                cells_out[2 * pos] = mask;
+                cells_out[2 * pos + 1] = vol;
+            }
+        }
+    }
     __device__ __forceinline__ uint64_t C(int n, int k) const { return B[n * kBinomCols + k]; }
     // |[base, base+size) n [rb, re)|
     __device__ __forceinline__ uint64_t isect(uint64_t base, uint64_t size) const {
@@ -288,7 +300,9 @@ __device__ __forceinline__ void leaf_test(const int64_t (&x)[NPL], const int64_t
             acc.ties += 1;                         // would-be cell on a tie (reading Z3)
         } else {
             acc.cells += 1;
-            acc.add_vol((uint64_t)(xj < 0 ? -xj : xj) / gabs);   // |det V_sigma|
+            const uint64_t vol = (uint64_t)(xj < 0 ? -xj : xj) / gabs;   // |det V_sigma|
+            acc.add_vol(vol);
+            cx.emit(inP | (1ull << j), vol);
         }
     }
 }
@@ -512,7 +526,9 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
                 acc.ties += 1;                     // would-be cell on a tie (reading Z3)
             } else {
                 acc.cells += 1;
-                acc.add_vol((uint64_t)(xj < 0 ? -xj : xj) / gabs);   // |det V_sigma|
+                const uint64_t vol = (uint64_t)(xj < 0 ? -xj : xj) / gabs;   // |det V_sigma|
+                acc.add_vol(vol);
+                cx.emit(inP | (1ull << c) | (1ull << j), vol);
             }
         }
     }
@@ -826,6 +842,9 @@ k_enumerate(LaunchArgs a) {
 
     cx.D = a.P.D;
     cx.deg_only = a.degree_only != 0;
+    cx.cells_out = a.cells_out;
+    cx.cells_cnt = a.cells_cnt;
+    cx.cells_cap = a.cells_cap;
     cx.kd = K - a.P.D;
     cx.fmin = (a.P.D > T) ? K - a.P.D : S + 1;
     cx.mytop = 0;

@@ -257,3 +257,59 @@ def test_degree_only_table3(table3):
         A, b = W.master_space_system(*mk)
         r = B.degree(A, b, seed=1, flags=0x40)
         assert r.degree == table3[mk][0] and r.candidates == r.total_candidates
+
+
+def test_cell_emission_matches_oracle():
+    # the emitted cells (index sets and NVol) are the oracle's
+    from oracle import cell_list
+    for (V, w, K) in [(W.c5_points(1, n_points=14, dim=4) + (5,)),
+                      (W.c5_points(3, n_points=24, dim=3) + (4,))]:
+        plan = B.Plan.from_points(V, w)
+        assert plan.cells() == cell_list(K, V, w)
+    A, b = W.master_space_system(2, 2)
+    lift = W.liftings(len(A) + 1, 1)
+    K, V, w = point_configuration(A, b, lift)["cone"]
+    got = B.Plan.from_system(A, b, lift).cells()
+    assert got == cell_list(K, V, w) and len(got) == 14
+
+
+@pytest.mark.parametrize("name", ["twisted_cubic", "dp0", "W1_5", "W2_2", "W2_3", "rnc9"])
+def test_walk_matches_enumeration(name):
+    # walking the subdivision finds exactly the enumerated cells
+    A, b = W.named_system(name)
+    lift = W.liftings(len(A) + 1, 1)
+    o, _ = _oracle_system(A, b, lift)
+    r = B.Plan.from_system(A, b, lift).degree_walk()
+    assert (r.degree, r.cells) == (o["volume"], o["cells"])
+
+
+def test_walk_points_and_c2():
+    for (V, w, K) in [(W.c5_points(1, n_points=14, dim=4) + (5,)),
+                      (W.c5_points(2, n_points=36, dim=5) + (6,)),
+                      (W.c5_points(3, n_points=64, dim=3) + (4,))]:
+        o = enumerate_range(K, V, w, threads=8)
+        r = B.Plan.from_points(V, w).degree_walk()
+        assert (r.degree, r.cells) == (o["volume"], o["cells"])
+    for s in (5, 31):
+        A, b, lift = W.c2_system(s)
+        o, _ = _oracle_system(A, b, lift)
+        r = B.Plan.from_system(A, b, lift).degree_walk()
+        assert (r.degree, r.cells) == (o["volume"], o["cells"])
+
+
+def test_walk_full_c5_and_table3(table3):
+    V, w = W.c5_points(1)
+    full = B.Plan.from_points(V, w).degree()
+    walk = B.Plan.from_points(V, w).degree_walk()
+    assert (walk.degree, walk.cells) == (full.degree, full.cells) == (51983602, 5152)
+    for mk in [(2, 4), (3, 3), (2, 5), (3, 4), (2, 6)]:
+        A, b = W.master_space_system(*mk)
+        r = B.Plan.from_system(A, b, seed=1).degree_walk()
+        assert r.degree == table3[mk][0], mk
+
+
+def test_walk_degenerate_lifting():
+    V, _ = W.c5_points(4, n_points=10, dim=3)
+    with pytest.raises(B.BdegError) as ei:
+        B.Plan.from_points(V, [7] * 10).degree_walk()
+    assert ei.value.status == 3

@@ -374,3 +374,22 @@ def test_c2_components_and_invariance():
         r1 = degree(A, b, lift)
         r2 = degree(A, b, W.liftings(13, 77))
         assert r1["degree"] == r2["degree"] and r1["ties"] == 0
+
+
+def test_cell_list_is_a_subdivision():
+    # Def. 1: the cells cover conv S with disjoint interiors, so
+    # their volumes add up to NVol (route 2) and every cell is affinely
+    # independent (NVol >= 1)
+    from oracle import cell_list
+    for seed in range(8):
+        pts, _ = W.random_point_set(300 + seed, 2 + seed % 2, 9, -2, 2)
+        pts = list(dict.fromkeys(pts))
+        d = len(pts[0])
+        if rank_fraction([[p[t] - pts[0][t] for t in range(d)] for p in pts]) < d:
+            continue
+        V = [(1,) + p for p in pts]
+        w = W.liftings(len(V), 900 + seed)
+        cells = cell_list(d + 1, V, w)
+        assert all(v >= 1 for _, v in cells)
+        assert sum(v for _, v in cells) == nvol_pulling(pts)
+        assert len(cells) == enumerate_lifted(d + 1, V, w)["cells"]
