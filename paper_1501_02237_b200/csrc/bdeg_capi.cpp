@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <cstring>
@@ -31,6 +32,8 @@ struct bdeg_plan_s {
     std::vector<int> point_of_var;
     int tier = 0, S = 0, T = 0, D = 0;
     int bits_v = 30, bits_l = 31;
+    bool big = false;                 // N > 64: walk only (rank space beyond uint64 / lane slots)
+    uint64_t basis_lo = 0, basis_hi = 0;   // basis-seeded start cell (N > 64, generated lifting)
     uint64_t nblocks = 0, total = 0;
     uint64_t seed_used = 0;
     int relifts = 0;
@@ -210,17 +213,81 @@ void choose_tier_and_blocks(bdeg_plan_s *p) {
     p->nblocks = C(p->binom, p->N - p->K + p->D, p->D);
 }
 
+// Greedy basis of the point vectors (first K linearly independent points,
+// exact rank test by fraction-free elimination in __int128).
+bool greedy_basis(const bdeg_plan_s *p, std::vector<int> &basis) {
+    const int K = p->K;
+    std::vector<std::vector<i128>> rows;   // reduced basis vectors (echelon)
+    std::vector<int> lead;
+    basis.clear();
+    for (int l = 0; l < p->N && (int)basis.size() < K; ++l) {
+        std::vector<i128> v(K);
+        for (int i = 0; i < K; ++i) v[i] = p->V[(size_t)l * K + i];
+        for (size_t r = 0; r < rows.size(); ++r) {
+            const int c = lead[r];
+            if (v[c] == 0) continue;
+            const i128 a = rows[r][c], b = v[c];
+            for (int i = 0; i < K; ++i) {
+                i128 t1, t2;
+                if (__builtin_mul_overflow(a, v[i], &t1) || __builtin_mul_overflow(b, rows[r][i], &t2)) return false;
+                v[i] = t1 - t2;
+            }
+            i128 g = 0;                           // keep entries small
+            for (int i = 0; i < K; ++i) { i128 x = v[i] < 0 ? -v[i] : v[i]; while (x) { i128 t = g % x; g = x; x = t; } }
+            if (g > 1) for (int i = 0; i < K; ++i) v[i] /= g;
+        }
+        int c = -1;
+        for (int i = 0; i < K; ++i) if (v[i] != 0) { c = i; break; }
+        if (c < 0) continue;
+        rows.push_back(v);
+        lead.push_back(c);
+        basis.push_back(l);
+    }
+    return (int)basis.size() == K;
+}
+
+// N > 64 with a generated lifting: lift a basis at 0 and every other point
+// at >= 1.  The hyperplane through the lifted basis is then h = 0 (a basis
+// spans everything), every other point is strictly above it, so the basis is
+// a cell of the regular subdivision: the walk's start cell (the degree does
+// not depend on the lifting).
+void seed_basis_lifting(bdeg_plan_s *p) {
+    if (!p->big || p->user_lift) return;
+    std::vector<int> basis;
+    if (!greedy_basis(p, basis)) return;
+    for (int64_t &w : p->w) if (w < 1) w = 1;
+    p->basis_lo = p->basis_hi = 0;
+    for (int l : basis) {
+        p->w[l] = 0;
+        if (l < 64) p->basis_lo |= 1ull << l; else p->basis_hi |= 1ull << (l - 64);
+    }
+}
+
 bdeg_status finish_plan(bdeg_plan_s *p) {
-    if (p->K > kMaxK || p->N > kMaxN)
-        return fail(p, BDEG_E_TOO_LARGE, "point configuration exceeds N <= 64, K <= 32 (N=" +
+    if (p->K > kMaxK || p->N > kMaxNWalk)
+        return fail(p, BDEG_E_TOO_LARGE, "point configuration exceeds N <= 128, K <= 32 (N=" +
                                               std::to_string(p->N) + ", K=" + std::to_string(p->K) + ")");
+    p->big = p->N > kMaxN;
     for (int64_t v : p->V)
         if (v > ((int64_t)1 << 40) || v < -((int64_t)1 << 40))
             return fail(p, BDEG_E_TOO_LARGE, "point coordinate beyond 2^40");
     for (int64_t v : p->w)
         if (v > ((int64_t)1 << 52) || v < -((int64_t)1 << 52))
             return fail(p, BDEG_E_TOO_LARGE, "lifting value beyond 2^52");
-    choose_tier_and_blocks(p);
+    if (p->big) {
+        // walk only: no rank space (C(N,K) may exceed 2^64), no enumeration items
+        int bv = 0, bl = 0;
+        sample_bits(p, bv, bl);
+        p->bits_v = std::min(30, std::max(bv + 2, 8));
+        p->bits_l = 61 - p->bits_v;
+        p->tier = (bv <= 28 && bl <= 28) ? 0 : ((bv + 2 <= 30 && bl < p->bits_l) ? 1 : 2);
+        p->total = 0;
+        p->S = p->T = p->D = 0;
+        p->nblocks = 0;
+        seed_basis_lifting(p);
+    } else {
+        choose_tier_and_blocks(p);
+    }
     p->l_dirty = true;
     return BDEG_OK;
 }
@@ -338,7 +405,8 @@ bdeg_status ensure_device(bdeg_plan_s *p) {
 // blocks) accumulating into `slots` (zeroed here).
 bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long long *slots, int rank,
                           int world, int force_tier, unsigned long long *cells_out = nullptr,
-                          unsigned long long *cells_cnt = nullptr, uint64_t cells_cap = 0) {
+                          unsigned long long *cells_cnt = nullptr, uint64_t cells_cap = 0,
+                          bool first_cell_search = false) {
     cudaStream_t st = (cudaStream_t)p->opt.stream;
     cudaError_t ce;
     if ((ce = cudaMemsetAsync(slots, 0, kNSlots * 8, st)) != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
@@ -367,6 +435,10 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     a.cells_out = cells_out;
     a.cells_cnt = cells_cnt;
     a.cells_cap = cells_cap;
+    if (first_cell_search) {            // any one cell, as fast as possible
+        a.degree_only = 1;
+        a.stop_on_cell = 1;
+    }
     a.bits_l = p->bits_l;
     a.replay = 0;
     a.counter = p->d_ctr + 0;
@@ -455,7 +527,8 @@ struct DevBuf {
 
 // Cells (mask, |det|) of ranks [b, e) into host memory (tier 2: no replays,
 // so nothing is emitted twice).
-bdeg_status cells_range(bdeg_plan_s *p, uint64_t b, uint64_t e, uint64_t *h_out, uint64_t cap, uint64_t *count) {
+bdeg_status cells_range(bdeg_plan_s *p, uint64_t b, uint64_t e, uint64_t *h_out, uint64_t cap, uint64_t *count,
+                        bool first_cell_search = false) {
     bdeg_status s = ensure_device(p);
     if (s) return s;
     cudaStream_t st = (cudaStream_t)p->opt.stream;
@@ -463,7 +536,7 @@ bdeg_status cells_range(bdeg_plan_s *p, uint64_t b, uint64_t e, uint64_t *h_out,
     if (!buf.alloc((2 * std::max<uint64_t>(cap, 1)) * 8) || !cnt.alloc(8))
         return fail(p, BDEG_E_CUDA, "cudaMalloc failed");
     cudaMemsetAsync(cnt.p, 0, 8, st);
-    s = enqueue_range(p, b, e, p->d_slots, 0, 1, 2, buf.u(), cnt.u(), cap);
+    s = enqueue_range(p, b, e, p->d_slots, 0, 1, 2, buf.u(), cnt.u(), cap, first_cell_search);
     if (s) return s;
     uint64_t n = 0;
     cudaMemcpyAsync(&n, cnt.p, 8, cudaMemcpyDeviceToHost, st);
@@ -484,72 +557,106 @@ uint64_t pow2_at_least(uint64_t x) {
     return c;
 }
 
-// One breadth-first walk of the subdivision.
+// One breadth-first walk of the subdivision.  Cell masks are
+// 16-byte {lo, hi} pairs.
 bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
     cudaStream_t st = (cudaStream_t)p->opt.stream;
     const double t0 = now_ms();
-    // 1. a starting cell from the enumeration kernel over a growing rank prefix
-    uint64_t start = 0;
-    {
-        uint64_t pair[2 * 16];
-        for (uint64_t L = 1ull << 16;; L *= 8) {
-            uint64_t n = 0;
-            bdeg_status s = cells_range(p, 0, std::min(L, p->total), pair, 16, &n);
-            if (s) return s;
-            if (n > 0) { start = pair[0]; break; }
-            if (L >= p->total) return fail(p, BDEG_E_DEGENERATE, "no cell found (degenerate lifting)");
-        }
+    uint64_t start[2] = {0, 0};
+    if (p->big) {
+        // basis-seeded lifting: the basis is a cell by construction
+        if (p->user_lift || (p->basis_lo == 0 && p->basis_hi == 0))
+            return fail(p, BDEG_E_INVALID, "N > 64 needs a generated lifting (basis-seeded start cell)");
+        start[0] = p->basis_lo;
+        start[1] = p->basis_hi;
+    } else {
+        // a starting cell: the enumeration kernel over the whole rank space in
+        // degree-only mode (cell-dead subtrees skipped), stopping at the first
+        // cell any warp verifies (tier 2: no replays, exact)
+        uint64_t pair[2 * 64];
+        uint64_t n = 0;
+        bdeg_status s = cells_range(p, 0, p->total, pair, 64, &n, true);
+        if (s) return s;
+        if (n == 0) return fail(p, BDEG_E_DEGENERATE, "no cell found (degenerate lifting)");
+        start[0] = pair[0];
     }
-    // 2. the walk
+    const double t_start = now_ms();
+    const bool dbg = std::getenv("BDEG_DEBUG") != nullptr;
     const int K = p->K;
-    uint64_t cap = 1ull << 20, ncur = 1, total_cells = 1;
+    int levels = 0;
+    uint64_t cap = 1ull << 20, ncur = 1, total_cells = 1, ccap = 1 << 16, ncap = 1 << 16;
     DevBuf table, cur, nxt, aux;
-    if (!table.alloc(cap * 8) || !cur.alloc(cap * 8) || !nxt.alloc(cap * 8) || !aux.alloc(16 * 8))
+    if (!table.alloc(cap * 16) || !cur.alloc(ccap * 16) || !nxt.alloc(ncap * 16) || !aux.alloc(16 * 8))
         return fail(p, BDEG_E_CUDA, "cudaMalloc failed");
     unsigned long long *next_cnt = aux.u(), *counter = aux.u() + 1, *stats = aux.u() + 2;   // stats: 8 slots
-    cudaMemsetAsync(table.p, 0, cap * 8, st);
-    const uint64_t h0 = walk_hash(start) & (cap - 1);
-    cudaMemcpyAsync(table.u() + h0, &start, 8, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(cur.p, &start, 8, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(table.p, 0, cap * 16, st);
+    const uint64_t h0 = walk_hash(start[0], start[1]) & (cap - 1);
+    cudaMemcpyAsync((char *)table.p + h0 * 16, start, 16, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(cur.p, start, 16, cudaMemcpyHostToDevice, st);
     const int grid = std::max(1, dev_info(p->opt.device).sms) * 4;
+    // int64 fast path of the ridge elimination: the plan's tier bounds
+    // (tier 0: 2^31 / 2^31, tier 1: 2^Bv / 2^Bl); tier 2 plans go wide at once
+    const int64_t limV = p->tier == 2 ? 0 : (int64_t)1 << (p->tier == 0 ? 30 : p->bits_v);
+    const int64_t limL = p->tier == 2 ? 0 : (int64_t)1 << (p->tier == 0 ? 31 : p->bits_l);
     uint64_t ridges = 0, boundary = 0;
+    auto grow_table = [&](uint64_t ncap_t) -> bdeg_status {
+        DevBuf t2;
+        if (!t2.alloc(ncap_t * 16)) return fail(p, BDEG_E_CUDA, "cudaMalloc (hash set grow) failed");
+        cudaMemsetAsync(t2.p, 0, ncap_t * 16, st);
+        cudaMemsetAsync(stats, 0, 8 * 8, st);
+        int rc = launch_rehash(table.p, cap, t2.p, ncap_t, stats + 3, st);
+        if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
+        cudaStreamSynchronize(st);
+        std::swap(table.p, t2.p);
+        cap = ncap_t;
+        return BDEG_OK;
+    };
     while (ncur > 0) {
-        if ((total_cells + ncur * K) * 2 > cap) {               // grow: rehash + bigger frontiers
-            const uint64_t ncap = pow2_at_least(4 * (total_cells + ncur * K));
-            DevBuf t2, c2;
-            if (!t2.alloc(ncap * 8) || !c2.alloc(ncap * 8)) return fail(p, BDEG_E_CUDA, "cudaMalloc (grow) failed");
-            cudaMemsetAsync(t2.p, 0, ncap * 8, st);
-            cudaMemsetAsync(stats, 0, 8 * 8, st);
-            int rc = launch_rehash(table.u(), cap, t2.u(), ncap, stats + 3, st);
-            if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
-            cudaMemcpyAsync(c2.p, cur.p, ncur * 8, cudaMemcpyDeviceToDevice, st);
-            cudaStreamSynchronize(st);
-            std::swap(table.p, t2.p);
-            std::swap(cur.p, c2.p);
-            if (!nxt.alloc(ncap * 8)) return fail(p, BDEG_E_CUDA, "cudaMalloc (grow) failed");
-            cap = ncap;
+        // hash set at load <= 1/2 for the expected growth; re-run on overflow
+        if ((total_cells + 3 * ncur) * 2 > cap) {
+            bdeg_status s = grow_table(pow2_at_least(3 * (total_cells + 3 * ncur)));
+            if (s) return s;
+        }
+        if (ncur * K > ncap) {                     // next frontier: <= ncur * K cells
+            ncap = pow2_at_least(ncur * K);
+            if (!nxt.alloc(ncap * 16)) return fail(p, BDEG_E_CUDA, "cudaMalloc (frontier) failed");
         }
         cudaMemsetAsync(aux.p, 0, 16 * 8, st);
-        int rc = launch_walk(p->d_L, K, p->N, cur.u(), ncur, nxt.u(), next_cnt, table.u(), cap, counter, stats,
-                             grid, st);
-        if (rc) return fail(p, BDEG_E_CUDA, std::string("k_walk: ") + cudaGetErrorString((cudaError_t)rc));
         uint64_t h[10];
-        cudaMemcpyAsync(h, aux.p, 10 * 8, cudaMemcpyDeviceToHost, st);
-        cudaError_t ce = cudaStreamSynchronize(st);
-        if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+        for (int attempt = 0;; ++attempt) {
+            int rc = launch_walk(p->d_L, K, p->N, cur.p, ncur, nxt.p, next_cnt, table.p, cap, counter, stats,
+                                 grid, st, limV, limL);
+            if (rc) return fail(p, BDEG_E_CUDA, std::string("k_walk: ") + cudaGetErrorString((cudaError_t)rc));
+            cudaMemcpyAsync(h, aux.p, 10 * 8, cudaMemcpyDeviceToHost, st);
+            cudaError_t ce = cudaStreamSynchronize(st);
+            if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+            if (h[2 + 3] == 0) break;
+            // full: keep the cells already appended, grow, redo the level
+            if (attempt > 4) return fail(p, BDEG_E_TOO_LARGE, "cell walk: hash set overflow");
+            bdeg_status s = grow_table(cap * 4);
+            if (s) return s;
+            cudaMemsetAsync(counter, 0, 8, st);
+            cudaMemsetAsync(stats, 0, 8 * 8, st);
+        }
         const uint64_t *sv = h + 2;
         ridges += sv[0];
         boundary += sv[5];
         if (sv[1] > 0) return fail(p, BDEG_E_DEGENERATE, "degenerate lifting: a ridge has a tie (cell walk)");
-        if (sv[2] > 0 || sv[4] > 0 || sv[3] > 0)
-            return fail(p, BDEG_E_TOO_LARGE, "cell walk: inconsistent ridge, value overflow or full table");
+        if (sv[2] > 0 || sv[4] > 0)
+            return fail(p, BDEG_E_TOO_LARGE, "cell walk: inconsistent ridge or value overflow");
         std::swap(cur.p, nxt.p);
+        std::swap(ccap, ncap);
         ncur = h[0];
         total_cells += ncur;
+        ++levels;
     }
-    // 3. exact volumes, one determinant per cell
+    if (dbg)
+        fprintf(stderr, "[bdeg walk] start cell %.2f ms, %d levels, walk %.2f ms, cells %llu, cap %llu\n",
+                t_start - t0, levels, now_ms() - t_start, (unsigned long long)total_cells,
+                (unsigned long long)cap);
+    // exact volumes, one determinant per cell
     cudaMemsetAsync(aux.p, 0, 16 * 8, st);
-    int rc = launch_cellvol(p->d_L, K, p->N, table.u(), cap, aux.u() + 8, aux.u(), grid, st);
+    int rc = launch_cellvol(p->d_L, K, p->N, table.p, cap, aux.u() + 8, aux.u(), grid, st, limV, limL);
     if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
     uint64_t h[16];
     cudaMemcpyAsync(h, aux.p, 16 * 8, cudaMemcpyDeviceToHost, st);
@@ -696,6 +803,7 @@ bdeg_status bdeg_relift(bdeg_plan_t p, int32_t attempt) {
     gen_lifting(p->seed_used, count, p->opt.lift_bits, p->lift);
     if (p->points_mode) p->w = p->lift;
     else rebuild_points(p);
+    seed_basis_lifting(p);
     p->relifts = attempt;
     p->l_dirty = true;
     return BDEG_OK;
@@ -703,6 +811,7 @@ bdeg_status bdeg_relift(bdeg_plan_t p, int32_t attempt) {
 
 bdeg_status bdeg_degree(bdeg_plan_t p, bdeg_result *out) {
     if (!p || !out) return fail(p, BDEG_E_INVALID, "NULL argument");
+    if (p->big) return fail(p, BDEG_E_TOO_LARGE, "N > 64: rank-space enumeration unavailable, use bdeg_degree_walk");
     const double t0 = now_ms();
     bdeg_result r;
     fill_front(p, &r);
@@ -735,6 +844,7 @@ bdeg_status bdeg_degree(bdeg_plan_t p, bdeg_result *out) {
 
 bdeg_status bdeg_degree_range(bdeg_plan_t p, uint64_t begin, uint64_t end, bdeg_result *out) {
     if (!p || !out) return fail(p, BDEG_E_INVALID, "NULL argument");
+    if (p->big) return fail(p, BDEG_E_TOO_LARGE, "N > 64: rank-space enumeration unavailable, use bdeg_degree_walk");
     const double t0 = now_ms();
     bdeg_result r;
     fill_front(p, &r);
@@ -756,6 +866,7 @@ bdeg_status bdeg_degree_range(bdeg_plan_t p, uint64_t begin, uint64_t end, bdeg_
 
 bdeg_status bdeg_degree_partial(bdeg_plan_t p, int64_t *d_slots) {
     if (!p || !d_slots) return fail(p, BDEG_E_INVALID, "NULL argument");
+    if (p->big) return fail(p, BDEG_E_TOO_LARGE, "N > 64: rank-space enumeration unavailable, use bdeg_degree_walk");
     if (p->K == 0) {
         cudaError_t ce = cudaMemsetAsync(d_slots, 0, kNSlots * 8, (cudaStream_t)p->opt.stream);
         return ce == cudaSuccess ? BDEG_OK : fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
@@ -808,6 +919,7 @@ bdeg_status bdeg_cells(bdeg_plan_t p, uint64_t begin, uint64_t end, uint64_t *h_
                        uint64_t *count) {
     if (!p || !count) return fail(p, BDEG_E_INVALID, "NULL argument");
     *count = 0;
+    if (p->big) return fail(p, BDEG_E_TOO_LARGE, "N > 64: rank-space enumeration unavailable");
     if (p->K == 0) return BDEG_OK;
     return cells_range(p, begin, end, h_out, capacity, count);
 }

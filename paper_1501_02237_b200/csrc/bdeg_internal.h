@@ -78,6 +78,7 @@ struct LaunchArgs {
     unsigned long long *cells_out;    // optional (mask, |det|) output of the cells found
     unsigned long long *cells_cnt;
     uint64_t cells_cap;
+    int stop_on_cell;                 // warps stop taking items once a cell was emitted
     void *stream;
 };
 
@@ -102,15 +103,17 @@ int enumerate_max_ctas_per_sm(const LaunchArgs &a);
 
 uint64_t launch_counter_add(uint64_t k);
 
-// ---- cell walk, bdeg_walk.cu
+// ---- cell walk, bdeg_walk.cu.  Cell masks are 128-bit
+// {lo, hi} pairs (N <= 128); device buffers hold 16 bytes per mask.
+constexpr int kMaxNWalk = 128;
 size_t walk_smem_bytes(int K, int N);
-uint64_t walk_hash(uint64_t key);
-int launch_walk(const int64_t *L, int K, int N, const unsigned long long *cur, uint64_t ncur,
-                unsigned long long *next, unsigned long long *next_cnt, unsigned long long *table, uint64_t cap,
-                unsigned long long *counter, unsigned long long *stats, int grid, void *stream);
-int launch_cellvol(const int64_t *L, int K, int N, const unsigned long long *table, uint64_t cap,
-                   unsigned long long *out, unsigned long long *counter, int grid, void *stream);
-int launch_rehash(const unsigned long long *old, uint64_t oldcap, unsigned long long *tab, uint64_t cap,
-                  unsigned long long *full_flag, void *stream);
+uint64_t walk_hash(uint64_t lo, uint64_t hi);
+int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, void *next,
+                unsigned long long *next_cnt, void *table, uint64_t cap, unsigned long long *counter,
+                unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL);
+int launch_cellvol(const int64_t *L, int K, int N, const void *table, uint64_t cap, unsigned long long *out,
+                   unsigned long long *counter, int grid, void *stream, int64_t limV, int64_t limL);
+int launch_rehash(const void *old, uint64_t oldcap, void *tab, uint64_t cap, unsigned long long *full_flag,
+                  void *stream);
 
 }  // namespace bdeg

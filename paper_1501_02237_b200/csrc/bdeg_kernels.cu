@@ -855,6 +855,7 @@ k_enumerate(LaunchArgs a) {
     const uint64_t nwork = a.replay ? (uint64_t)min((unsigned long long)a.ovf_cap, *a.ovf_count)
                                     : (span > a.blk_offset ? (span - a.blk_offset + a.blk_stride - 1) / a.blk_stride : 0);
     for (;;) {
+        if (a.stop_on_cell && *(volatile unsigned long long *)a.cells_cnt > 0) break;
         unsigned long long idx = 0;
         if (lane == 0) idx = atomicAdd(a.counter, 1ull);
         idx = __shfl_sync(FULL, idx, 0);

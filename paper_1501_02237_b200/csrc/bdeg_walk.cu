@@ -82,13 +82,65 @@ __device__ __forceinline__ int nth_bit(uint64_t m, int t) {
     return t < pl ? (int)__fns(lo, 0, t + 1) : 32 + (int)__fns(hi, 0, t + 1 - pl);
 }
 
+// Cell / ridge masks over up to 128 points (bit l = point l).
+struct M128 {
+    uint64_t lo, hi;
+};
+__device__ __forceinline__ bool mbit(const M128 &m, int l) {
+    return ((l < 64 ? m.lo >> l : m.hi >> (l - 64)) & 1ull) != 0;
+}
+__device__ __forceinline__ M128 mclear(M128 m, int l) {
+    if (l < 64) m.lo &= ~(1ull << l); else m.hi &= ~(1ull << (l - 64));
+    return m;
+}
+__device__ __forceinline__ M128 mset(M128 m, int l) {
+    if (l < 64) m.lo |= 1ull << l; else m.hi |= 1ull << (l - 64);
+    return m;
+}
+__device__ __forceinline__ int mpopc(const M128 &m) { return __popcll(m.lo) + __popcll(m.hi); }
+__device__ __forceinline__ int mnth(const M128 &m, int t) {
+    const int pl = __popcll(m.lo);
+    return t < pl ? nth_bit(m.lo, t) : 64 + nth_bit(m.hi, t - pl);
+}
+__device__ __forceinline__ int mtop(const M128 &m) {
+    return m.hi ? 127 - __clzll((long long)m.hi) : 63 - __clzll((long long)m.lo);
+}
+__device__ __forceinline__ uint64_t mhash(const M128 &m) { return mix64(m.lo ^ mix64(m.hi + 0x9E3779B97F4A7C15ull)); }
+
+// 128-bit compare-and-swap (sm_90+: ATOMG.E.CAS.128)
+__device__ __forceinline__ M128 cas128(M128 *addr, M128 cmp, M128 val) {
+    M128 old;
+    asm volatile("{\n\t.reg .b128 c, n, o;\n\t"
+                 "mov.b128 c, {%2, %3};\n\t"
+                 "mov.b128 n, {%4, %5};\n\t"
+                 "atom.global.cas.b128 o, [%6], c, n;\n\t"
+                 "mov.b128 {%0, %1}, o;\n\t}"
+                 : "=l"(old.lo), "=l"(old.hi)
+                 : "l"(cmp.lo), "l"(cmp.hi), "l"(val.lo), "l"(val.hi), "l"(addr)
+                 : "memory");
+    return old;
+}
+
+__device__ __forceinline__ int64_t qdiv64(int64_t num, const Div &dv) {
+    if (dv.unit == 1) return num;
+    if (dv.unit == -1) return -num;
+    return (int64_t)((uint64_t)(num >> dv.tz) * dv.inv);
+}
+__device__ __forceinline__ bool inside(int64_t v, int64_t lim) {
+    return (uint64_t)(v + (lim - 1)) <= (uint64_t)(2 * (lim - 1));
+}
+
 // Eliminate the pivot columns of `piv_mask` (ascending order) from the lifted
 // matrix in the warp's scratch scr[i*NP + l] (rows 0..K, K = lift row).
 // Afterwards the single alive V row is *vrow; values are the true minors.
+// WIDE = false: int64 numerators, every stored value checked against
+// |V| < limV, |lift| < limL (limV * limL <= 2^61, limV^2 <= 2^61: numerators
+// exact) — ovf set if a value leaves the bounds; WIDE = true: int128
+// numerators, quotients verified, |v| < 2^62.
 // Returns false if the pivots are linearly dependent.
-template <int NPL>
-__device__ bool eliminate(const int64_t *Lsm, int64_t *scr, int K, int N, uint64_t piv_mask, int lane,
-                          int *vrow, int64_t *last_piv, bool &ovf) {
+template <int NPL, bool WIDE>
+__device__ bool eliminate(const int64_t *Lsm, int64_t *scr, int K, int N, M128 piv_mask, int lane,
+                          int *vrow, int64_t *last_piv, bool &ovf, int64_t limV, int64_t limL) {
     constexpr int NP = 32 * NPL;
     __syncwarp();
     for (int i = 0; i <= K; ++i)
@@ -100,56 +152,84 @@ __device__ bool eliminate(const int64_t *Lsm, int64_t *scr, int K, int N, uint64
     __syncwarp();
     uint64_t alive = (K >= 64) ? ~0ull : ((1ull << K) - 1);
     int64_t prev = 1;
-    const int T = __popcll(piv_mask);
+    const int T = mpopc(piv_mask);
     for (int t = 0; t < T; ++t) {
-        const int p = nth_bit(piv_mask, t);
+        const int p = mnth(piv_mask, t);
         const bool nz = lane < K && ((alive >> lane) & 1ull) && scr[lane * NP + p] != 0;
         const unsigned bal = __ballot_sync(FULL, nz);
         if (bal == 0) return false;
         const int r = __ffs(bal) - 1;
         const int64_t piv = scr[r * NP + p];
         const Div dv = make_div(prev);
+        int64_t prow[NPL];
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) prow[q] = scr[r * NP + lane + 32 * q];
         for (int i = 0; i <= K; ++i) {
             if (i == r || (i < K && !((alive >> i) & 1ull))) continue;
             const int64_t ci = scr[i * NP + p];
+            const int64_t lim = i < K ? limV : limL;
 #pragma unroll
             for (int q = 0; q < NPL; ++q) {
                 const int l = lane + 32 * q;
                 if (l == p) continue;
-                scr[i * NP + l] = qdiv((i128)piv * scr[i * NP + l] - (i128)ci * scr[r * NP + l], dv, ovf);
+                if constexpr (WIDE) {
+                    scr[i * NP + l] = qdiv((i128)piv * scr[i * NP + l] - (i128)ci * prow[q], dv, ovf);
+                } else {
+                    const int64_t v = qdiv64(piv * scr[i * NP + l] - ci * prow[q], dv);
+                    ovf |= !inside(v, lim);
+                    scr[i * NP + l] = v;
+                }
             }
         }
         alive &= ~(1ull << r);
         prev = piv;
         __syncwarp();
+        if constexpr (!WIDE) {
+            if (__any_sync(FULL, ovf)) return true;       // caller redoes it wide
+        }
     }
     *vrow = __ffsll((long long)alive) - 1;
     *last_piv = prev;
     return true;
 }
 
+template <int NPL>
+__device__ __forceinline__ bool eliminate_auto(const int64_t *Lsm, int64_t *scr, int K, int N, M128 piv_mask,
+                                               int lane, int *vrow, int64_t *last_piv, bool &ovf, int64_t limV,
+                                               int64_t limL) {
+    if (limV > 0) {
+        bool o = false;
+        const bool ok = eliminate<NPL, false>(Lsm, scr, K, N, piv_mask, lane, vrow, last_piv, o, limV, limL);
+        if (!__any_sync(FULL, o)) return ok;
+    }
+    return eliminate<NPL, true>(Lsm, scr, K, N, piv_mask, lane, vrow, last_piv, ovf, 0, 0);
+}
+
 struct WalkArgs {
     const int64_t *L;             // lifted matrix, column-major (K+1) x N
     int K, N;
-    const unsigned long long *cur;    // frontier (cell masks)
+    const M128 *cur;                  // frontier (cell masks)
     uint64_t ncur;
-    unsigned long long *next;         // next frontier
+    M128 *next;                       // next frontier
     unsigned long long *next_cnt;
-    unsigned long long *table;        // hash set of cell masks (0 = empty)
+    M128 *table;                      // hash set of cell masks ({0,0} = empty)
     uint64_t cap;                     // power of two
     unsigned long long *counter;      // work counter
+    int64_t limV, limL;               // int64 fast-path bounds (0: always int128)
     unsigned long long *stats;        // [0] ridges tested, [1] ties, [2] inconsistent,
                                       // [3] table full, [4] overflow, [5] boundary ridges
     int grid;
     void *stream;
 };
 
-__device__ __forceinline__ bool insert(unsigned long long *table, uint64_t cap, uint64_t key, bool &full) {
-    uint64_t h = mix64(key) & (cap - 1);
-    for (uint64_t probe = 0; probe < cap; ++probe) {
-        const unsigned long long old = atomicCAS(table + h, 0ull, (unsigned long long)key);
-        if (old == 0ull) return true;
-        if (old == key) return false;
+__device__ __forceinline__ bool insert(M128 *table, uint64_t cap, M128 key, bool &full) {
+    uint64_t h = mhash(key) & (cap - 1);
+    const M128 empty = {0, 0};
+    const uint64_t max_probe = cap < 4096 ? cap : 4096;   // load <= 1/2: short probes
+    for (uint64_t probe = 0; probe < max_probe; ++probe) {
+        const M128 old = cas128(table + h, empty, key);
+        if (old.lo == 0 && old.hi == 0) return true;
+        if (old.lo == key.lo && old.hi == key.hi) return false;
         h = (h + 1) & (cap - 1);
     }
     full = true;
@@ -169,7 +249,6 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int NP = 32 * NPL;
     int64_t *scr = reinterpret_cast<int64_t *>(smem + ((lsz * 8 + 15) & ~15)) + (size_t)warp * (K + 1) * NP;
-    const uint64_t nmask = (N >= 64) ? ~0ull : ((1ull << N) - 1);
     unsigned long long st[6] = {0, 0, 0, 0, 0, 0};
     const uint64_t nwork = a.ncur * (uint64_t)K;
     for (;;) {
@@ -177,14 +256,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
         if (lane == 0) idx = atomicAdd(a.counter, 1ull);
         idx = __shfl_sync(FULL, idx, 0);
         if (idx >= nwork) break;
-        const uint64_t m = a.cur[idx / K];
-        const int p = nth_bit(m, (int)(idx % K));
-        const uint64_t ridge = m & ~(1ull << p);
+        const M128 m = a.cur[idx / K];
+        const int p = mnth(m, (int)(idx % K));
+        const M128 ridge = mclear(m, p);
         bool ovf = false;
         int vr = 0;
         int64_t g = 1;
         ++st[0];
-        if (!eliminate<NPL>(Lsm, scr, K, N, ridge, lane, &vr, &g, ovf)) { ++st[2]; continue; }
+        if (!eliminate_auto<NPL>(Lsm, scr, K, N, ridge, lane, &vr, &g, ovf, a.limV, a.limL)) { ++st[2]; continue; }
         int64_t x[NPL], yk[NPL];
         bool valid[NPL];
         const int kappa = g > 0 ? 1 : -1;
@@ -193,11 +272,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
             const int l = lane + 32 * q;
             x[q] = scr[vr * NP + l];
             yk[q] = kappa > 0 ? scr[K * NP + l] : -scr[K * NP + l];
-            valid[q] = ((nmask & ~ridge) >> l) & 1ull;
+            valid[q] = l < N && !mbit(ridge, l);
         }
         if (__any_sync(FULL, ovf)) { ++st[4]; continue; }
         // side of the current cell's point p; the neighbour is on the other side
-        const int64_t xp = __shfl_sync(FULL, (long long)(p >= 32 && NPL > 1 ? x[NPL - 1] : x[0]), p & 31);
+        int64_t xps = x[0];
+#pragma unroll
+        for (int q = 1; q < NPL; ++q) if ((p >> 5) == q) xps = x[q];
+        const int64_t xp = __shfl_sync(FULL, (long long)xps, p & 31);
         if (xp == 0) { ++st[2]; continue; }
         const bool want_pos = xp < 0;
         // points of span(R) strictly below: R is no lower ridge -> inconsistent
@@ -215,20 +297,23 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
         if (__any_sync(FULL, bad0)) { ++st[2]; continue; }
         const uint32_t mk = __reduce_min_sync(FULL, kk);
         if (mk == 0xFFFFFFFFu) { ++st[5]; continue; }      // boundary ridge
-        uint64_t cand = 0;
+        uint32_t cand[NPL];
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
             const bool side = want_pos ? x[q] > 0 : x[q] < 0;
-            cand |= (uint64_t)__ballot_sync(FULL, valid[q] && side && key[q] <= mk + 64u) << (32 * q);
+            cand[q] = __ballot_sync(FULL, valid[q] && side && key[q] <= mk + 64u);
         }
         int found = -1;
         bool tie = false;
-        while (cand) {
-            const int j = __ffsll((long long)cand) - 1;
-            cand &= cand - 1;
-            const bool js = NPL > 1 && j >= 32;
-            const int64_t xj = __shfl_sync(FULL, (long long)(js ? x[NPL - 1] : x[0]), j & 31);
-            const int64_t yj = __shfl_sync(FULL, (long long)(js ? yk[NPL - 1] : yk[0]), j & 31);
+        for (int cq = 0; cq < NPL; ++cq)
+        while (cand[cq]) {
+            const int j = 32 * cq + __ffs(cand[cq]) - 1;
+            cand[cq] &= cand[cq] - 1;
+            int64_t xs = x[0], ys = yk[0];
+#pragma unroll
+            for (int q = 1; q < NPL; ++q) if ((j >> 5) == q) { xs = x[q]; ys = yk[q]; }
+            const int64_t xj = __shfl_sync(FULL, (long long)xs, j & 31);
+            const int64_t yj = __shfl_sync(FULL, (long long)ys, j & 31);
             bool bad = false, zero = false;
 #pragma unroll
             for (int q = 0; q < NPL; ++q) {
@@ -247,7 +332,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
         if (tie) ++st[1];
         if (found < 0) { if (!tie) ++st[5]; continue; }
         if (lane == 0) {
-            const uint64_t nm = ridge | (1ull << found);
+            const M128 nm = mset(ridge, found);
             bool full = false;
             if (insert(a.table, a.cap, nm, full)) {
                 const unsigned long long pos = atomicAdd(a.next_cnt, 1ull);
@@ -264,9 +349,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
 // |det| of every cell in the table (one warp per cell) into 4 limbs + count
 template <int NPL>
 __global__ void __launch_bounds__(kWarps * 32) k_cellvol(const int64_t *L, int K, int N,
-                                                          const unsigned long long *table, uint64_t cap,
+                                                          const M128 *table, uint64_t cap,
                                                           unsigned long long *out /* [4 limbs, cells, ovf] */,
-                                                          unsigned long long *counter) {
+                                                          unsigned long long *counter, int64_t limV, int64_t limL) {
     extern __shared__ __align__(16) unsigned char smem[];
     int64_t *Lsm = reinterpret_cast<int64_t *>(smem);
     const int lsz = (K + 1) * N;
@@ -283,14 +368,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellvol(const int64_t *L, int K
         base = __shfl_sync(FULL, base, 0);
         if (base >= cap) break;
         for (uint64_t s = base; s < base + chunk && s < cap; ++s) {
-            const uint64_t m = table[s];
-            if (m == 0) continue;
-            const int top = 63 - __clzll((long long)m);
+            const M128 m = table[s];
+            if (m.lo == 0 && m.hi == 0) continue;
+            const int top = mtop(m);
             bool ovf = false;
             int vr = 0;
             int64_t g = 1;
-            if (!eliminate<NPL>(Lsm, scr, K, N, m & ~(1ull << top), lane, &vr, &g, ovf)) { ++ovfs; continue; }
-            const int64_t d = scr[vr * NP + top];            // +-det of the cell
+            if (!eliminate_auto<NPL>(Lsm, scr, K, N, mclear(m, top), lane, &vr, &g, ovf, limV, limL)) {
+                ++ovfs;
+                continue;
+            }
+            const int64_t d = scr[vr * NP + top];            // +-det of the cell (column top)
             if (__any_sync(FULL, ovf)) { ++ovfs; continue; }
             const uint64_t v = (uint64_t)(d < 0 ? -d : d);
             const uint64_t t = lo + v;
@@ -309,11 +397,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellvol(const int64_t *L, int K
     }
 }
 
-__global__ void k_rehash(const unsigned long long *old, uint64_t oldcap, unsigned long long *tab, uint64_t cap,
+__global__ void k_rehash(const M128 *old, uint64_t oldcap, M128 *tab, uint64_t cap,
                          unsigned long long *full_flag) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < oldcap; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = old[i];
-        if (k == 0) continue;
+        const M128 k = old[i];
+        if (k.lo == 0 && k.hi == 0) continue;
         bool full = false;
         insert(tab, cap, k, full);
         if (full) atomicAdd(full_flag, 1ull);
@@ -322,61 +410,81 @@ __global__ void k_rehash(const unsigned long long *old, uint64_t oldcap, unsigne
 
 }  // namespace walk
 
-uint64_t walk_hash(uint64_t key) {          // host copy of the device hash (for seeding)
-    uint64_t z = key;
+// host copy of the device hash of a 128-bit cell mask (for seeding the table)
+static uint64_t hmix(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     return z ^ (z >> 31);
 }
+uint64_t walk_hash(uint64_t lo, uint64_t hi) { return hmix(lo ^ hmix(hi + 0x9E3779B97F4A7C15ull)); }
 
-int launch_rehash(const unsigned long long *old, uint64_t oldcap, unsigned long long *tab, uint64_t cap,
-                  unsigned long long *full_flag, void *stream) {
-    walk::k_rehash<<<1184, 256, 0, (cudaStream_t)stream>>>(old, oldcap, tab, cap, full_flag);
+int launch_rehash(const void *old, uint64_t oldcap, void *tab, uint64_t cap, unsigned long long *full_flag,
+                  void *stream) {
+    walk::k_rehash<<<1184, 256, 0, (cudaStream_t)stream>>>((const walk::M128 *)old, oldcap, (walk::M128 *)tab, cap,
+                                                           full_flag);
     launch_counter_add(1);
     return (int)cudaGetLastError();
 }
+
+static int npl_of(int N) { return (N + 31) / 32; }
 
 size_t walk_smem_bytes(int K, int N) {
-    const int npl = N > 32 ? 2 : 1;
-    return (((size_t)(K + 1) * N * 8 + 15) & ~(size_t)15) + (size_t)walk::kWarps * (K + 1) * 32 * npl * 8;
+    return (((size_t)(K + 1) * N * 8 + 15) & ~(size_t)15) + (size_t)walk::kWarps * (K + 1) * 32 * npl_of(N) * 8;
 }
 
-int launch_walk(const int64_t *L, int K, int N, const unsigned long long *cur, uint64_t ncur,
-                unsigned long long *next, unsigned long long *next_cnt, unsigned long long *table, uint64_t cap,
-                unsigned long long *counter, unsigned long long *stats, int grid, void *stream) {
+template <int NPL>
+static int walk_npl(const walk::WalkArgs &a, int grid, size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)walk::k_walk<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    walk::k_walk<NPL><<<grid, walk::kWarps * 32, smem, (cudaStream_t)a.stream>>>(a);
+    return (int)cudaGetLastError();
+}
+
+int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, void *next,
+                unsigned long long *next_cnt, void *table, uint64_t cap, unsigned long long *counter,
+                unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL) {
     walk::WalkArgs a;
-    a.L = L; a.K = K; a.N = N; a.cur = cur; a.ncur = ncur; a.next = next; a.next_cnt = next_cnt;
-    a.table = table; a.cap = cap; a.counter = counter; a.stats = stats; a.grid = grid; a.stream = stream;
+    a.limV = limV;
+    a.limL = limL;
+    a.L = L; a.K = K; a.N = N; a.cur = (const walk::M128 *)cur; a.ncur = ncur; a.next = (walk::M128 *)next;
+    a.next_cnt = next_cnt; a.table = (walk::M128 *)table; a.cap = cap; a.counter = counter; a.stats = stats;
+    a.grid = grid; a.stream = stream;
     const size_t smem = walk_smem_bytes(K, N);
-    cudaError_t e;
-    if (N > 32) {
-        e = cudaFuncSetAttribute((const void *)walk::k_walk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        walk::k_walk<2><<<grid, walk::kWarps * 32, smem, (cudaStream_t)stream>>>(a);
-    } else {
-        e = cudaFuncSetAttribute((const void *)walk::k_walk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        walk::k_walk<1><<<grid, walk::kWarps * 32, smem, (cudaStream_t)stream>>>(a);
+    int rc;
+    switch (npl_of(N)) {
+        case 1: rc = walk_npl<1>(a, grid, smem); break;
+        case 2: rc = walk_npl<2>(a, grid, smem); break;
+        case 3: rc = walk_npl<3>(a, grid, smem); break;
+        default: rc = walk_npl<4>(a, grid, smem); break;
     }
     launch_counter_add(1);
+    return rc;
+}
+
+template <int NPL>
+static int cellvol_npl(const int64_t *L, int K, int N, const void *table, uint64_t cap, unsigned long long *out,
+                       unsigned long long *counter, int grid, void *stream, int64_t limV, int64_t limL, size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)walk::k_cellvol<NPL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    walk::k_cellvol<NPL><<<grid, walk::kWarps * 32, smem, (cudaStream_t)stream>>>(
+        L, K, N, (const walk::M128 *)table, cap, out, counter, limV, limL);
     return (int)cudaGetLastError();
 }
 
-int launch_cellvol(const int64_t *L, int K, int N, const unsigned long long *table, uint64_t cap,
-                   unsigned long long *out, unsigned long long *counter, int grid, void *stream) {
+int launch_cellvol(const int64_t *L, int K, int N, const void *table, uint64_t cap, unsigned long long *out,
+                   unsigned long long *counter, int grid, void *stream, int64_t limV, int64_t limL) {
     const size_t smem = walk_smem_bytes(K, N);
-    cudaError_t e;
-    if (N > 32) {
-        e = cudaFuncSetAttribute((const void *)walk::k_cellvol<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        walk::k_cellvol<2><<<grid, walk::kWarps * 32, smem, (cudaStream_t)stream>>>(L, K, N, table, cap, out, counter);
-    } else {
-        e = cudaFuncSetAttribute((const void *)walk::k_cellvol<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        walk::k_cellvol<1><<<grid, walk::kWarps * 32, smem, (cudaStream_t)stream>>>(L, K, N, table, cap, out, counter);
+    int rc;
+    switch (npl_of(N)) {
+        case 1: rc = cellvol_npl<1>(L, K, N, table, cap, out, counter, grid, stream, limV, limL, smem); break;
+        case 2: rc = cellvol_npl<2>(L, K, N, table, cap, out, counter, grid, stream, limV, limL, smem); break;
+        case 3: rc = cellvol_npl<3>(L, K, N, table, cap, out, counter, grid, stream, limV, limL, smem); break;
+        default: rc = cellvol_npl<4>(L, K, N, table, cap, out, counter, grid, stream, limV, limL, smem); break;
     }
     launch_counter_add(1);
-    return (int)cudaGetLastError();
+    return rc;
 }
 
 }  // namespace bdeg

@@ -131,3 +131,20 @@ def test_finalize_exact_limbs():
     s2 = pack_slots((1 << 40) - 1, 2, 0, 6)
     tot = [a + b for a, b in zip(s1, s2)]
     assert p.finalize(tot).degree == 2 * ((1 << 40) - 1)
+
+
+def test_big_configuration_plans_walk_only():
+    # N > 64 (W_{3,8}: N = 72, K = 26; Table 3's ">=" entries): the planner
+    # accepts it for the cell walk, the rank-space entry points refuse
+    A, b = W.master_space_system(3, 8)
+    p = B.Plan.from_system(A, b, seed=1)
+    info = p.info()
+    assert (info.K, info.N) == (26, 72) and info.total_candidates == 0
+    for call in (p.degree, lambda: p.degree_range(0, 10), lambda: p.cells(0, 10)):
+        with pytest.raises(B.BdegError) as ei:
+            call()
+        assert ei.value.status == BB.BDEG_E_TOO_LARGE
+    # a user lifting cannot seed the walk's start cell for N > 64
+    q = B.Plan.from_system(A, b, lifting=W.liftings(len(A) + 1, 2))
+    with pytest.raises(B.BdegError):
+        q.degree_walk()
