@@ -182,7 +182,7 @@ def run_gpu(args):
     total = math.comb(len(V), K)
     stream = torch.cuda.current_stream()
 
-    plan = B.Plan.from_points(V, w, rank=rank, world=world, stream=stream.cuda_stream)
+    plan = B.Plan.from_points(V, w, rank=rank, world=world, stream=stream.cuda_stream, device=local)
     plan.use_torch_workspace(local)
     info = plan.info()
     slots = torch.zeros(B.NSLOTS, dtype=torch.int64, device=dev)
@@ -236,7 +236,7 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        with B.Plan.from_points(V, w, rank=rank, world=world, stream=stream.cuda_stream) as p2:
+        with B.Plan.from_points(V, w, rank=rank, world=world, stream=stream.cuda_stream, device=local) as p2:
             if world == 1:
                 r2 = p2.degree()
             else:

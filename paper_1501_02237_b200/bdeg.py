@@ -184,8 +184,20 @@ def _result(r: _Result) -> Result:
                   kernel_ms=r.kernel_ms, total_ms=r.total_ms)
 
 
-def _options(seed=1, lift_bits=20, max_relift=32, device=0, rank=0, world=1, stream=None,
+def _current_device():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:  # noqa: BLE001 - torch is plumbing only
+        pass
+    return 0
+
+
+def _options(seed=1, lift_bits=20, max_relift=32, device=None, rank=0, world=1, stream=None,
              flags=0, inner_levels=-1, ctas_per_sm=0) -> _Options:
+    if device is None:      # the caller's current CUDA device (one process per GPU)
+        device = _current_device()
     o = _Options()
     lib.bdeg_default_options(ctypes.byref(o))
     o.seed = seed & ((1 << 64) - 1)

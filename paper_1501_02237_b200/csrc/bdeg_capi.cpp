@@ -346,11 +346,18 @@ void pool_put(int d, void *ptr, size_t bytes) {
 
 bdeg_status ensure_device(bdeg_plan_s *p) {
     cudaError_t e;
+    if (p->dev_ready || p->opt.device >= 0) {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= p->opt.device)
+            return fail(p, BDEG_E_CUDA, "no CUDA device available (libbdeg has no CPU fallback)");
+        // every device entry point runs on the plan's device (one process may drive several)
+        if ((e = cudaSetDevice(p->opt.device)) != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
+    }
     if (!p->dev_ready) {
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= p->opt.device)
             return fail(p, BDEG_E_CUDA, "no CUDA device available (libbdeg has no CPU fallback)");
-        if ((e = cudaSetDevice(p->opt.device)) != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
+
         const DevInfo &di = dev_info(p->opt.device);
         if (!di.ok) return fail(p, BDEG_E_CUDA, "cudaGetDeviceProperties failed");
         if (di.major < 10) return fail(p, BDEG_E_CUDA, "libbdeg is built for sm_100a (B200); device is older");

@@ -186,34 +186,32 @@ struct WAcc {
 
 struct Ctx {
     const uint64_t *B;   // binomial table in smem
+    const LaunchArgs *A; // the kernel's (grid-constant) arguments: rarely used fields
     int N, K, lane;
-    uint64_t rb, re;
     int64_t limV, limL;  // tier-1 bounds (exclusive)
     uint64_t nmask;      // points 0..N-1
     int D, kd, fmin;     // item depth, K - D, smallest forced DFS level
     int mytop;           // this lane's entry of the item tuple: c_{kd + lane} (lane < D)
-    uint64_t irb, ire;   // the item's candidates n [rb, re)
+    uint64_t irb, ire;   // the item's candidates n [rank_begin, rank_end)
     bool deg_only;       // skip cell-dead subtrees (singular count becomes a lower bound)
-    bool partial;
-    unsigned long long *cells_out;   // optional (mask, |det|) pairs of the cells found
-    unsigned long long *cells_cnt;
-    uint64_t cells_cap;
-    __device__ __forceinline__ void emit(uint64_t mask, uint64_t vol) const {
-        if (cells_out && lane == 0) {
-            const unsigned long long pos = atomicAdd(cells_cnt, 1ull);
-            if (pos < cells_cap) {
-                cells_out[2 * pos] = mask;
-                cells_out[2 * pos + 1] = vol;
-            }
-        }
-    }
+    bool partial;        // the item is cut by the rank range
     __device__ __forceinline__ uint64_t C(int n, int k) const { return B[n * kBinomCols + k]; }
-    // |[base, base+size) n [rb, re)|
+    // |[base, base+size) n [irb, ire)| (subtrees below the item level lie inside the item)
     __device__ __forceinline__ uint64_t isect(uint64_t base, uint64_t size) const {
         if (!partial) return size;
-        uint64_t lo = base > rb ? base : rb;
-        uint64_t hi = base + size < re ? base + size : re;
+        uint64_t lo = base > irb ? base : irb;
+        uint64_t hi = base + size < ire ? base + size : ire;
         return hi > lo ? hi - lo : 0;
+    }
+    // optional emission of a found cell
+    __device__ __forceinline__ void emit(uint64_t mask, uint64_t vol) const {
+        if (A->cells_out && lane == 0) {
+            const unsigned long long pos = atomicAdd(A->cells_cnt, 1ull);
+            if (pos < A->cells_cap) {
+                A->cells_out[2 * pos] = mask;
+                A->cells_out[2 * pos + 1] = vol;
+            }
+        }
     }
 };
 
@@ -234,8 +232,8 @@ __device__ __forceinline__ void leaf_test(const int64_t (&x)[NPL], const int64_t
                                           const Ctx &cx, Acc &acc) {
     int jlo = 0, jhi = c1;
     if (cx.partial) {
-        if (cx.rb > base) jlo = (cx.rb - base >= (uint64_t)c1) ? c1 : (int)(cx.rb - base);
-        if (cx.re < base + (uint64_t)c1) jhi = (cx.re <= base) ? 0 : (int)(cx.re - base);
+        if (cx.irb > base) jlo = (cx.irb - base >= (uint64_t)c1) ? c1 : (int)(cx.irb - base);
+        if (cx.ire < base + (uint64_t)c1) jhi = (cx.ire <= base) ? 0 : (int)(cx.ire - base);
         if (jlo >= jhi) return;
     }
     acc.cand += (uint64_t)(jhi - jlo);
@@ -598,7 +596,7 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
             // loops are index-bounded, so garbage values cannot hang the warp
             elim_step<TIER, NPL, RV>(sv, sl, cv, cl, pr, piv, dv, cx, ov, ol, ovf);
             const uint64_t cinP = inP | (1ull << c);
-            const bool cdead = dead || node_dead<TIER, NPL, RV - 1>(ov, ol, cinP, (int64_t)piv, cx);
+            const bool cdead = cx.deg_only && (dead || node_dead<TIER, NPL, RV - 1>(ov, ol, cinP, (int64_t)piv, cx));
             if (cdead && cx.deg_only) {          // no cell in the subtree: skip it
                 acc.cand += (i >= cx.fmin) ? cx.ire - cx.irb : cx.isect(nb, ns);
                 continue;
@@ -650,8 +648,9 @@ __device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, co
     {
         // effective range = item n [rb, re).  A forced level's subtree spans
         // other items too: its dependent-prefix count is clamped to [irb, ire).
-        const uint64_t lo = tall > cx0.rb ? tall : cx0.rb;
-        const uint64_t hi = tall + isize < cx0.re ? tall + isize : cx0.re;
+        const uint64_t rb = cx0.A->rank_begin, re = cx0.A->rank_end;
+        const uint64_t lo = tall > rb ? tall : rb;
+        const uint64_t hi = tall + isize < re ? tall + isize : re;
         if (hi <= lo) return;
         cx.irb = lo;
         cx.ire = hi;
@@ -762,7 +761,7 @@ __device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, co
         for (int q = 0; q < NPL; ++q) { xx[q] = (int64_t)sv[q][0]; yy[q] = (int64_t)sl[q]; }
         leaf_test<NPL>(xx, yy, ctop, ttop, inP, prev > 0 ? 1 : -1, 1, cx, acc);
     } else {
-        const bool dead = node_dead<TIER, NPL, S + 1>(sv, sl, inP, prev, cx);
+        const bool dead = cx.deg_only && node_dead<TIER, NPL, S + 1>(sv, sl, inP, prev, cx);
         if (dead && cx.deg_only) {
             acc.cand += cx.ire - cx.irb;
             return;
@@ -783,7 +782,7 @@ template <int TIER, int NPL, int S>
 #define BDEG_MIN_BLOCKS (S >= 5 ? 3 : 4)
 #endif
 __global__ void __launch_bounds__(kWarps * 32, BDEG_MIN_BLOCKS)
-k_enumerate(LaunchArgs a) {
+k_enumerate(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int K = a.P.K, N = a.P.N, T = a.P.T;
     (void)T;
@@ -832,8 +831,7 @@ k_enumerate(LaunchArgs a) {
     cx.N = N;
     cx.K = K;
     cx.lane = lane;
-    cx.rb = a.rank_begin;
-    cx.re = a.rank_end;
+    cx.A = &a;
     cx.partial = true;
     cx.limV = (int64_t)1 << a.bits_v;
     cx.limL = (int64_t)1 << a.bits_l;
@@ -842,9 +840,6 @@ k_enumerate(LaunchArgs a) {
 
     cx.D = a.P.D;
     cx.deg_only = a.degree_only != 0;
-    cx.cells_out = a.cells_out;
-    cx.cells_cnt = a.cells_cnt;
-    cx.cells_cap = a.cells_cap;
     cx.kd = K - a.P.D;
     cx.fmin = (a.P.D > T) ? K - a.P.D : S + 1;
     cx.mytop = 0;
@@ -940,14 +935,16 @@ static KernFn pick(int tier, int npl, int S) {
 // cudaFuncSetAttribute(max dynamic smem) once per (kernel, size): the value
 // only ever grows, so remember the largest one set per kernel
 static std::mutex g_attr_mu;
-static std::map<KernFn, size_t> g_attr;
+static std::map<std::pair<int, KernFn>, size_t> g_attr;   // (device, kernel) -> smem set
 
 static cudaError_t ensure_smem_attr(KernFn f, size_t smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_attr_mu);
-    auto it = g_attr.find(f);
+    auto it = g_attr.find({dev, f});
     if (it != g_attr.end() && it->second >= smem) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) g_attr[f] = smem;
+    if (e == cudaSuccess) g_attr[{dev, f}] = smem;
     return e;
 }
 
