@@ -175,6 +175,13 @@ bdeg_status bdeg_degree_partial(bdeg_plan_t plan, int64_t *d_slots);
 bdeg_status bdeg_cells(bdeg_plan_t plan, uint64_t begin, uint64_t end, uint64_t *h_out, uint64_t capacity,
                        uint64_t *count);
 
+/* The lifted hyperplane of a cell (host): h with h . v_c = omega_c for the K
+ * points c of the cell, returned as h = h_num / den (h_num: K int64, den =
+ * +-det V_sigma).  In the paper's notation the cell's
+ * inner normal is alpha^ = (alpha, 1) with, for the generic formulation
+ * v = (1, a): h = (<a^_0, alpha^>, -alpha).  BDEG_E_TOO_LARGE beyond int64. */
+bdeg_status bdeg_cell_normal(bdeg_plan_t plan, uint64_t mask_lo, uint64_t mask_hi, int64_t *h_num, int64_t *den);
+
 /* output-sensitive degree: walk the regular subdivision cell to
  * cell across ridges (the paper's pivoting, and its graph view,
  * P:1068-1132), each pivot an exact warp-wide ridge test, cells deduplicated

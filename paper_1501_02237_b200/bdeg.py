@@ -83,7 +83,7 @@ EXPORTS = ["bdeg_default_options", "bdeg_plan", "bdeg_plan_points", "bdeg_plan_i
            "bdeg_workspace_bytes", "bdeg_set_workspace", "bdeg_degree", "bdeg_degree_range",
            "bdeg_degree_partial", "bdeg_finalize", "bdeg_relift", "bdeg_last_error",
            "bdeg_status_str", "bdeg_destroy", "bdeg_launch_count", "bdeg_num_items",
-           "bdeg_item_range", "bdeg_cells", "bdeg_degree_walk"]
+           "bdeg_item_range", "bdeg_cells", "bdeg_degree_walk", "bdeg_cell_normal"]
 
 
 def _load():
@@ -121,6 +121,9 @@ def _load():
                                ctypes.c_uint64, P(ctypes.c_uint64)]
     lib.bdeg_cells.restype = ctypes.c_int
     lib.bdeg_degree_walk.argtypes = [plan_t, P(_Result)]
+    lib.bdeg_cell_normal.argtypes = [plan_t, ctypes.c_uint64, ctypes.c_uint64, P(ctypes.c_int64),
+                                     P(ctypes.c_int64)]
+    lib.bdeg_cell_normal.restype = ctypes.c_int
     lib.bdeg_degree_walk.restype = ctypes.c_int
     lib.bdeg_launch_count.argtypes = []
     lib.bdeg_launch_count.restype = ctypes.c_uint64
@@ -346,6 +349,18 @@ class Plan:
             m, v = buf[2 * i], buf[2 * i + 1]
             out.append((tuple(l for l in range(64) if (m >> l) & 1), v))
         return sorted(out)
+
+    def cell_normal(self, cell):
+        """Exact lifted hyperplane h = h_num/den of a cell (point-index tuple):
+        h . v_c = omega_c on the cell (the paper's inner normal)."""
+        from fractions import Fraction
+        lo = sum(1 << l for l in cell if l < 64)
+        hi = sum(1 << (l - 64) for l in cell if l >= 64)
+        K = len(cell)
+        num = (ctypes.c_int64 * K)()
+        den = ctypes.c_int64()
+        _check(lib.bdeg_cell_normal(self._h, lo, hi, num, ctypes.byref(den)), self._h)
+        return [Fraction(num[i], den.value) for i in range(K)]
 
     def degree_range(self, begin: int, end: int) -> Result:
         r = _Result()

@@ -931,6 +931,53 @@ bdeg_status bdeg_cells(bdeg_plan_t p, uint64_t begin, uint64_t end, uint64_t *h_
     return cells_range(p, begin, end, h_out, capacity, count);
 }
 
+bdeg_status bdeg_cell_normal(bdeg_plan_t p, uint64_t mask_lo, uint64_t mask_hi, int64_t *h_num, int64_t *den) {
+    if (!p || !h_num || !den) return fail(p, BDEG_E_INVALID, "NULL argument");
+    const int K = p->K;
+    std::vector<int> idx;
+    for (int l = 0; l < p->N; ++l)
+        if (l < 64 ? ((mask_lo >> l) & 1ull) : ((mask_hi >> (l - 64)) & 1ull)) idx.push_back(l);
+    if ((int)idx.size() != K) return fail(p, BDEG_E_INVALID, "mask does not hold K points");
+    // solve V_sigma h = w_sigma (rows v_c) fraction-free: h = h~ / D, D = det V_sigma
+    // (Cramer's rule by Bareiss on the augmented matrix, exact in checked __int128)
+    std::vector<std::vector<i128>> M(K, std::vector<i128>(K + 1));
+    for (int r = 0; r < K; ++r) {
+        for (int t = 0; t < K; ++t) M[r][t] = p->V[(size_t)idx[r] * K + t];
+        M[r][K] = p->w[idx[r]];
+    }
+    i128 prev = 1;
+    int sign = 1;
+    for (int k = 0; k < K; ++k) {
+        int piv = -1;
+        for (int r = k; r < K; ++r) if (M[r][k] != 0) { piv = r; break; }
+        if (piv < 0) return fail(p, BDEG_E_INVALID, "singular cell");
+        if (piv != k) { std::swap(M[piv], M[k]); sign = -sign; }
+        for (int r = 0; r < K; ++r) {
+            if (r == k) continue;
+            for (int t = 0; t <= K; ++t) {
+                if (t == k) continue;
+                i128 a, b;
+                if (__builtin_mul_overflow(M[k][k], M[r][t], &a) || __builtin_mul_overflow(M[r][k], M[k][t], &b))
+                    return fail(p, BDEG_E_TOO_LARGE, "normal overflow");
+                M[r][t] = (a - b) / prev;       // exact (Gauss-Jordan Bareiss)
+            }
+            M[r][k] = 0;
+        }
+        prev = M[k][k];
+    }
+    // now M = diag(D,...,D | h~) with D = det (up to the row-swap sign)
+    const i128 D = M[K - 1][K - 1];
+    for (int t = 0; t < K; ++t) {
+        const i128 v = M[t][K];
+        if (v > INT64_MAX || v < INT64_MIN) return fail(p, BDEG_E_TOO_LARGE, "normal beyond int64");
+        h_num[t] = (int64_t)v;
+    }
+    if (D > INT64_MAX || D < INT64_MIN) return fail(p, BDEG_E_TOO_LARGE, "determinant beyond int64");
+    *den = (int64_t)D;
+    (void)sign;
+    return BDEG_OK;
+}
+
 bdeg_status bdeg_degree_walk(bdeg_plan_t p, bdeg_result *out) {
     if (!p || !out) return fail(p, BDEG_E_INVALID, "NULL argument");
     const double t0 = now_ms();

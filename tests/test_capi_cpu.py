@@ -148,3 +148,22 @@ def test_big_configuration_plans_walk_only():
     q = B.Plan.from_system(A, b, lifting=W.liftings(len(A) + 1, 2))
     with pytest.raises(B.BdegError):
         q.degree_walk()
+
+
+def test_cell_normal_matches_oracle_solve():
+    # bdeg_cell_normal: h with h . v_c = omega_c on the cell, exact
+    from oracle.subdivision import _solve, colex_unrank
+    V, w = W.c5_points(1, n_points=14, dim=4)
+    p = B.Plan.from_points(V, w)
+    rng = W.SplitMix64(5)
+    done = 0
+    for _ in range(40):
+        cell = colex_unrank(rng.uniform_int(0, math.comb(14, 5) - 1), 5)
+        det, h = _solve([list(V[c]) for c in cell], [w[c] for c in cell])
+        if det == 0:
+            with pytest.raises(B.BdegError):
+                p.cell_normal(cell)
+            continue
+        assert p.cell_normal(cell) == h
+        done += 1
+    assert done > 20

@@ -313,3 +313,20 @@ def test_walk_degenerate_lifting():
     with pytest.raises(B.BdegError) as ei:
         B.Plan.from_points(V, [7] * 10).degree_walk()
     assert ei.value.status == 3
+
+
+def test_emitted_cells_with_normals_are_lower_facets():
+    # f2: every emitted cell with its exact normal satisfies the lower-face
+    # system I(sigma) strictly and the NVol is |det V_sigma|
+    from fractions import Fraction
+    from oracle.snf import det_fraction
+    V, w = W.c5_points(2, n_points=30, dim=4)
+    plan = B.Plan.from_points(V, w)
+    cells = plan.cells()
+    assert len(cells) == enumerate_range(5, V, w, threads=8)["cells"]
+    for cell, vol in cells[:200]:
+        h = plan.cell_normal(cell)
+        for l in range(len(V)):
+            r = w[l] - sum(hi * vi for hi, vi in zip(h, V[l]))
+            assert (r == 0) if l in cell else (r > 0)
+        assert abs(det_fraction([list(V[c]) for c in cell])) == vol
