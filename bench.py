@@ -173,11 +173,19 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # BDEG_SHARE_GPU=1 (testing only): ranks share the visible GPUs round-robin
+    # and combine over gloo, to exercise the multi-rank path on a 1-GPU box
+    share = os.environ.get("BDEG_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     desc, K, V, w, extra = workload(args.workload)
     total = math.comb(len(V), K)
     stream = torch.cuda.current_stream()
@@ -253,6 +261,12 @@ def run_gpu(args):
         dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     e2e_step = float(e2e.item())
 
+    if rank == 0 and world > 1:
+        # the combined shards must equal a single-GPU run over the whole rank space
+        with B.Plan.from_points(V, w, stream=stream.cuda_stream, device=local) as p1:
+            full = p1.degree()
+        assert (full.degree, full.cells, full.candidates) == (res.degree, res.cells, res.candidates), \
+            "multi-GPU combine differs from the single-GPU result"
     if rank == 0:
         peaks, peak_kind = load_peaks()
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
