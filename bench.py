@@ -192,6 +192,10 @@ def run_gpu(args):
 
     plan = B.Plan.from_points(V, w, rank=rank, world=world, stream=stream.cuda_stream, device=local)
     plan.use_torch_workspace(local)
+    steal = world > 1 and os.environ.get("BDEG_STEAL", "1") == "1"
+    if steal:        # one global item queue over all GPUs (CUDA IPC + NVLink atomics)
+        from paper_1501_02237_b200.multi import enable_work_stealing
+        enable_work_stealing(plan, local)
     info = plan.info()
     slots = torch.zeros(B.NSLOTS, dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -294,7 +298,8 @@ def run_gpu(args):
             "config": {"workload": desc, "K": K, "N": len(V), "candidates": total,
                        "l2": "flushed between steps (256 MiB write outside the timed events)",
                        "inner_levels": info.inner_levels, "tier": info.tier,
-                       "parallelism": f"rank-space blocks interleaved over {world} GPU(s)", **extra},
+                       "parallelism": (f"rank-space work items from one cross-GPU queue (IPC, NVLink atomics) over {world} GPUs"
+                                       if steal else f"rank-space work items interleaved over {world} GPU(s)"), **extra},
             "time_to_degree_ms": e2e_step,
             "result": {"degree": res.degree, "cells": res.cells, "singular": res.singular,
                        "candidates": res.candidates, "ties": res.ties,

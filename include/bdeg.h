@@ -192,6 +192,19 @@ bdeg_status bdeg_cell_normal(bdeg_plan_t plan, uint64_t mask_lo, uint64_t mask_h
  * Re-lifts generated liftings on ties like bdeg_degree. */
 bdeg_status bdeg_degree_walk(bdeg_plan_t plan, bdeg_result *out);
 
+/* Cross-GPU dynamic work stealing.  One process (rank 0)
+ * creates a pair of item counters in its GPU's memory and exports them as a
+ * CUDA IPC handle (BDEG_STEAL_HANDLE_BYTES bytes); every rank (rank 0 included,
+ * via the same handle in another process, or its own) attaches them to its
+ * plan.  bdeg_degree_partial then takes work items from ONE global
+ * largest-first queue with system-scope atomics over NVLink instead of the
+ * static interleaved shard; the counters alternate by step parity and rank 0's
+ * launch zeroes the idle one, so all ranks must call bdeg_degree_partial once
+ * per step, separated by the result all-reduce (which orders the steps). */
+#define BDEG_STEAL_HANDLE_BYTES 64
+bdeg_status bdeg_steal_create(int32_t device, uint8_t *out_handle);
+bdeg_status bdeg_steal_attach(bdeg_plan_t plan, const uint8_t *handle);
+
 /* Carry-normalise summed slots (HOST memory) into *out. */
 bdeg_status bdeg_finalize(bdeg_plan_t plan, const int64_t *h_slots, bdeg_result *out);
 

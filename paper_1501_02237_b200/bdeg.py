@@ -83,7 +83,8 @@ EXPORTS = ["bdeg_default_options", "bdeg_plan", "bdeg_plan_points", "bdeg_plan_i
            "bdeg_workspace_bytes", "bdeg_set_workspace", "bdeg_degree", "bdeg_degree_range",
            "bdeg_degree_partial", "bdeg_finalize", "bdeg_relift", "bdeg_last_error",
            "bdeg_status_str", "bdeg_destroy", "bdeg_launch_count", "bdeg_num_items",
-           "bdeg_item_range", "bdeg_cells", "bdeg_degree_walk", "bdeg_cell_normal"]
+           "bdeg_item_range", "bdeg_cells", "bdeg_degree_walk", "bdeg_cell_normal",
+           "bdeg_steal_create", "bdeg_steal_attach"]
 
 
 def _load():
@@ -125,6 +126,10 @@ def _load():
                                      P(ctypes.c_int64)]
     lib.bdeg_cell_normal.restype = ctypes.c_int
     lib.bdeg_degree_walk.restype = ctypes.c_int
+    lib.bdeg_steal_create.argtypes = [ctypes.c_int32, ctypes.c_char_p]
+    lib.bdeg_steal_create.restype = ctypes.c_int
+    lib.bdeg_steal_attach.argtypes = [plan_t, ctypes.c_char_p]
+    lib.bdeg_steal_attach.restype = ctypes.c_int
     lib.bdeg_launch_count.argtypes = []
     lib.bdeg_launch_count.restype = ctypes.c_uint64
     for name in ["bdeg_plan", "bdeg_plan_points", "bdeg_plan_info", "bdeg_set_workspace",
@@ -135,6 +140,13 @@ def _load():
 
 
 lib = _load()
+
+
+def steal_create(device: int) -> bytes:
+    """Rank 0: allocate the cross-GPU item counters, return their IPC handle."""
+    buf = ctypes.create_string_buffer(64)
+    _check(lib.bdeg_steal_create(device, buf))
+    return buf.raw
 
 
 def launch_count() -> int:
@@ -306,6 +318,10 @@ class Plan:
         """Items of `rank` under bdeg_degree_partial's sharding rule."""
         n = self.num_items()
         return [n - 1 - (rank + i * world) for i in range((n - rank + world - 1) // world) if n - 1 - (rank + i * world) >= 0]
+
+    def steal_attach(self, handle: bytes):
+        """Take work items from the shared cross-GPU queue (bdeg_steal_attach)."""
+        _check(lib.bdeg_steal_attach(self._h, handle), self._h)
 
     def workspace_bytes(self) -> int:
         return int(lib.bdeg_workspace_bytes(self._h))

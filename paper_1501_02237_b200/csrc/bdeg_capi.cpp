@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <cstring>
 #include <string>
@@ -33,6 +34,8 @@ struct bdeg_plan_s {
     int tier = 0, S = 0, T = 0, D = 0;
     int bits_v = 30, bits_l = 31;
     bool big = false;                 // N > 64: walk only (rank space beyond uint64 / lane slots)
+    unsigned long long *steal = nullptr;   // cross-GPU item counters (2, by step parity), IPC-mapped
+    int steal_parity = 0;
     uint64_t basis_lo = 0, basis_hi = 0;   // basis-seeded start cell (N > 64, generated lifting)
     uint64_t nblocks = 0, total = 0;
     uint64_t seed_used = 0;
@@ -305,6 +308,7 @@ struct DevInfo { bool ok = false; int sms = 0, major = 0; };
 std::mutex g_mu;
 DevInfo g_dev[64];
 std::vector<std::pair<size_t, void *>> g_pool[64];
+std::map<std::string, void *> g_steal_local;   // IPC handles exported by this process
 
 const DevInfo &dev_info(int d) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -436,6 +440,14 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     a.ovf_cap = p->ovf_cap;
     a.grid = p->grid;
     a.stream = st;
+    if (p->steal && world > 1) {        // one global largest-first queue over all GPUs
+        a.counter = p->steal + p->steal_parity;
+        a.system_counter = 1;
+        a.blk_offset = 0;
+        a.blk_stride = 1;
+        if (rank == 0) a.reset_next = p->steal + (p->steal_parity ^ 1);
+        p->steal_parity ^= 1;
+    }
     a.tier = force_tier >= 0 ? force_tier : p->tier;
     a.bits_v = p->bits_v;
     a.degree_only = (p->opt.flags & BDEG_FLAG_DEGREE_ONLY) ? 1 : 0;
@@ -455,6 +467,8 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
         a.tier = 2;
         a.replay = 1;
         a.counter = p->d_ctr + 1;
+        a.system_counter = 0;
+        a.reset_next = nullptr;
         rc = launch_enumerate(a);
         if (rc) return fail(p, BDEG_E_CUDA, std::string("k_enumerate replay: ") + cudaGetErrorString((cudaError_t)rc));
     }
@@ -1007,6 +1021,45 @@ bdeg_status bdeg_degree_walk(bdeg_plan_t p, bdeg_result *out) {
     r.kernel_ms = kms;
     r.total_ms = now_ms() - t0;
     *out = r;
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_steal_create(int32_t device, uint8_t *out_handle) {
+    if (!out_handle) return fail(nullptr, BDEG_E_INVALID, "NULL argument");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(nullptr, BDEG_E_CUDA, cudaGetErrorString(e));
+    void *ptr = nullptr;
+    if ((e = cudaMalloc(&ptr, 256)) != cudaSuccess) return fail(nullptr, BDEG_E_CUDA, cudaGetErrorString(e));
+    if ((e = cudaMemset(ptr, 0, 256)) != cudaSuccess) return fail(nullptr, BDEG_E_CUDA, cudaGetErrorString(e));
+    cudaIpcMemHandle_t h;
+    if ((e = cudaIpcGetMemHandle(&h, ptr)) != cudaSuccess) return fail(nullptr, BDEG_E_CUDA, cudaGetErrorString(e));
+    static_assert(sizeof(h) == BDEG_STEAL_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(out_handle, &h, sizeof(h));
+    {   // the exporting process cannot IPC-open its own allocation: remember it
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_steal_local[std::string((const char *)out_handle, sizeof(h))] = ptr;
+    }
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_steal_attach(bdeg_plan_t p, const uint8_t *handle) {
+    if (!p || !handle) return fail(p, BDEG_E_INVALID, "NULL argument");
+    bdeg_status s = ensure_device(p);
+    if (s) return s;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void *ptr = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_steal_local.find(std::string((const char *)handle, sizeof(h)));
+        if (it != g_steal_local.end()) ptr = it->second;
+    }
+    if (!ptr) {
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return fail(p, BDEG_E_COMM, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    }
+    p->steal = (unsigned long long *)ptr;
+    p->steal_parity = 0;
     return BDEG_OK;
 }
 

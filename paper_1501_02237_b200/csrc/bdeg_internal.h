@@ -79,6 +79,8 @@ struct LaunchArgs {
     unsigned long long *cells_cnt;
     uint64_t cells_cap;
     int stop_on_cell;                 // warps stop taking items once a cell was emitted
+    unsigned long long *reset_next;   // cross-GPU stealing: counter of the next step, zeroed by rank 0
+    int system_counter;               // counter lives in a peer GPU (IPC): system-scope atomics
     void *stream;
 };
 

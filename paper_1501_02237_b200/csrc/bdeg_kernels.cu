@@ -849,10 +849,12 @@ k_enumerate(const __grid_constant__ LaunchArgs a) {
     const uint64_t span = a.blk_last - a.blk_first + 1;
     const uint64_t nwork = a.replay ? (uint64_t)min((unsigned long long)a.ovf_cap, *a.ovf_count)
                                     : (span > a.blk_offset ? (span - a.blk_offset + a.blk_stride - 1) / a.blk_stride : 0);
+    if (a.reset_next && blockIdx.x == 0 && threadIdx.x == 0) *a.reset_next = 0ull;   // next step's counter
     for (;;) {
         if (a.stop_on_cell && *(volatile unsigned long long *)a.cells_cnt > 0) break;
         unsigned long long idx = 0;
-        if (lane == 0) idx = atomicAdd(a.counter, 1ull);
+        if (lane == 0)
+            idx = a.system_counter ? atomicAdd_system(a.counter, 1ull) : atomicAdd(a.counter, 1ull);
         idx = __shfl_sync(FULL, idx, 0);
         if (idx >= nwork) break;
         const uint64_t blk = a.replay ? a.ovf_queue[idx] : (a.blk_last - (a.blk_offset + idx * a.blk_stride));

@@ -29,6 +29,16 @@ def all_reduce_slots(slots, group=None):
     return slots
 
 
+def enable_work_stealing(plan: Plan, device: int, group=None):
+    """All ranks draw work items from one queue in rank 0's GPU memory (CUDA
+    IPC + system-scope atomics over NVLink), instead of static shards."""
+    import torch.distributed as dist
+    from .bdeg import steal_create
+    obj = [steal_create(device) if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    plan.steal_attach(obj[0])     # rank 0 resolves its own handle locally
+
+
 def degree_distributed(plan: Plan, device, group=None) -> Result:
     """This rank's shard on `device`, one all-reduce, exact finalize."""
     import torch

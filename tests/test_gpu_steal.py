@@ -1,0 +1,66 @@
+"""Cross-GPU dynamic work stealing exercised with two processes
+sharing the one available GPU: rank 0 exports the item counters by CUDA IPC,
+both ranks draw work items from that single queue with system-scope atomics,
+one all-reduce (gloo here, NCCL on a multi-GPU box) combines the slots, and the
+result must equal a single-process run over the whole rank space."""
+import os
+import socket
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    import workloads as W
+    import paper_1501_02237_b200 as B
+    from paper_1501_02237_b200.multi import all_reduce_slots, enable_work_stealing
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    V, w = W.c5_points(1)
+    plan = B.Plan.from_points(V, w, rank=rank, world=world, device=0)
+    enable_work_stealing(plan, 0)
+    out = []
+    for _ in range(3):                       # several steps: counters alternate by parity
+        slots = torch.zeros(B.NSLOTS, dtype=torch.int64, device="cuda")
+        plan.degree_partial(slots.data_ptr())
+        torch.cuda.synchronize()
+        host = slots.cpu()
+        all_reduce_slots(host)
+        r = plan.finalize(host.tolist())
+        out.append((r.degree, r.cells, r.singular, r.candidates))
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+def test_two_ranks_share_one_queue():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    import workloads as W
+    import paper_1501_02237_b200 as B
+    V, w = W.c5_points(1)
+    full = B.Plan.from_points(V, w).degree()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    want = (full.degree, full.cells, full.singular, full.candidates)
+    assert all(step == want for r in (0, 1) for step in res[r])
