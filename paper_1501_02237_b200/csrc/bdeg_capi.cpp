@@ -440,14 +440,6 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     a.ovf_cap = p->ovf_cap;
     a.grid = p->grid;
     a.stream = st;
-    if (p->steal && world > 1) {        // one global largest-first queue over all GPUs
-        a.counter = p->steal + p->steal_parity;
-        a.system_counter = 1;
-        a.blk_offset = 0;
-        a.blk_stride = 1;
-        if (rank == 0) a.reset_next = p->steal + (p->steal_parity ^ 1);
-        p->steal_parity ^= 1;
-    }
     a.tier = force_tier >= 0 ? force_tier : p->tier;
     a.bits_v = p->bits_v;
     a.degree_only = (p->opt.flags & BDEG_FLAG_DEGREE_ONLY) ? 1 : 0;
@@ -461,6 +453,14 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     a.bits_l = p->bits_l;
     a.replay = 0;
     a.counter = p->d_ctr + 0;
+    if (p->steal && world > 1) {        // one global largest-first queue over all GPUs
+        a.counter = p->steal + p->steal_parity;
+        a.system_counter = 1;
+        a.blk_offset = 0;
+        a.blk_stride = 1;
+        if (rank == 0) a.reset_next = p->steal + (p->steal_parity ^ 1);
+        p->steal_parity ^= 1;
+    }
     int rc = launch_enumerate(a);
     if (rc) return fail(p, BDEG_E_CUDA, std::string("k_enumerate launch: ") + cudaGetErrorString((cudaError_t)rc));
     if (a.tier != 2) {   // re-run the blocks that left their tier, in int64/int128
