@@ -205,6 +205,16 @@ bdeg_status bdeg_degree_walk(bdeg_plan_t plan, bdeg_result *out);
 bdeg_status bdeg_steal_create(int32_t device, uint8_t *out_handle);
 bdeg_status bdeg_steal_attach(bdeg_plan_t plan, const uint8_t *handle);
 
+/* front end at scale (no plan needed).  Rank of A (n x m,
+ * ROW-major int64) modulo a prime < 2^32 by GPU Gaussian row reduction (the
+ * paper's GPU row reduction).  rank_p(A) <= rank_Q(A), equal
+ * unless p divides every maximal non-zero minor.  bdeg_dimension_modp returns
+ * n - max(rank_p) over the primes 2^31-1 and 2^31-19 (probabilistic, pinned by
+ * the paper's Tables 1-2; the exact dimension comes from bdeg_plan's SNF). */
+bdeg_status bdeg_rank_modp(int32_t n, int32_t m, const int64_t *A, uint32_t prime, int32_t device, void *stream,
+                           int64_t *rank);
+bdeg_status bdeg_dimension_modp(int32_t n, int32_t m, const int64_t *A, int32_t device, int32_t *dim);
+
 /* Carry-normalise summed slots (HOST memory) into *out. */
 bdeg_status bdeg_finalize(bdeg_plan_t plan, const int64_t *h_slots, bdeg_result *out);
 

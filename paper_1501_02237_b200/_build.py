@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbdeg.so")
-SOURCES = ["bdeg_kernels.cu", "bdeg_walk.cu", "bdeg_capi.cpp", "frontend.cpp"]
+SOURCES = ["bdeg_kernels.cu", "bdeg_walk.cu", "bdeg_rank.cu", "bdeg_capi.cpp", "frontend.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -84,7 +84,7 @@ EXPORTS = ["bdeg_default_options", "bdeg_plan", "bdeg_plan_points", "bdeg_plan_i
            "bdeg_degree_partial", "bdeg_finalize", "bdeg_relift", "bdeg_last_error",
            "bdeg_status_str", "bdeg_destroy", "bdeg_launch_count", "bdeg_num_items",
            "bdeg_item_range", "bdeg_cells", "bdeg_degree_walk", "bdeg_cell_normal",
-           "bdeg_steal_create", "bdeg_steal_attach"]
+           "bdeg_steal_create", "bdeg_steal_attach", "bdeg_rank_modp", "bdeg_dimension_modp"]
 
 
 def _load():
@@ -130,6 +130,12 @@ def _load():
     lib.bdeg_steal_create.restype = ctypes.c_int
     lib.bdeg_steal_attach.argtypes = [plan_t, ctypes.c_char_p]
     lib.bdeg_steal_attach.restype = ctypes.c_int
+    lib.bdeg_rank_modp.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int64), ctypes.c_uint32,
+                                   ctypes.c_int32, ctypes.c_void_p, P(ctypes.c_int64)]
+    lib.bdeg_rank_modp.restype = ctypes.c_int
+    lib.bdeg_dimension_modp.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int64), ctypes.c_int32,
+                                        P(ctypes.c_int32)]
+    lib.bdeg_dimension_modp.restype = ctypes.c_int
     lib.bdeg_launch_count.argtypes = []
     lib.bdeg_launch_count.restype = ctypes.c_uint64
     for name in ["bdeg_plan", "bdeg_plan_points", "bdeg_plan_info", "bdeg_set_workspace",
@@ -147,6 +153,16 @@ def steal_create(device: int) -> bytes:
     buf = ctypes.create_string_buffer(64)
     _check(lib.bdeg_steal_create(device, buf))
     return buf.raw
+
+
+def dimension_modp(A, device=None) -> int:
+    """dim V*(x^A - b) = n - rank A by GPU row reduction mod 2 primes."""
+    n = len(A)
+    m = len(A[0]) if n else 0
+    buf = _i64([A[i][j] for i in range(n) for j in range(m)])
+    d = ctypes.c_int32()
+    _check(lib.bdeg_dimension_modp(n, m, buf, _current_device() if device is None else device, ctypes.byref(d)))
+    return d.value
 
 
 def launch_count() -> int:

@@ -1063,6 +1063,30 @@ bdeg_status bdeg_steal_attach(bdeg_plan_t p, const uint8_t *handle) {
     return BDEG_OK;
 }
 
+bdeg_status bdeg_rank_modp(int32_t n, int32_t m, const int64_t *A, uint32_t prime, int32_t device, void *stream,
+                           int64_t *rank) {
+    if (!A || !rank || n < 1 || m < 0 || prime < 3) return fail(nullptr, BDEG_E_INVALID, "bad arguments");
+    if (m == 0) { *rank = 0; return BDEG_OK; }
+    const long long r = rank_modp(A, n, m, prime, device, stream);
+    if (r < 0) return fail(nullptr, BDEG_E_CUDA, "GPU row reduction failed (no CUDA device?)");
+    *rank = r;
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_dimension_modp(int32_t n, int32_t m, const int64_t *A, int32_t device, int32_t *dim) {
+    if (!dim) return fail(nullptr, BDEG_E_INVALID, "NULL argument");
+    const uint32_t primes[2] = {2147483647u, 2147483629u};   // 2^31 - 1, 2^31 - 19
+    int64_t best = 0;
+    for (uint32_t pr : primes) {
+        int64_t r = 0;
+        bdeg_status s = bdeg_rank_modp(n, m, A, pr, device, nullptr, &r);
+        if (s) return s;
+        best = std::max(best, r);
+    }
+    *dim = (int32_t)(n - best);
+    return BDEG_OK;
+}
+
 const char *bdeg_last_error(bdeg_plan_t p) { return p ? p->err.c_str() : g_err.c_str(); }
 
 const char *bdeg_status_str(bdeg_status s) {

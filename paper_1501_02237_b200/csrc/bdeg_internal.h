@@ -118,4 +118,7 @@ int launch_cellvol(const int64_t *L, int K, int N, const void *table, uint64_t c
 int launch_rehash(const void *old, uint64_t oldcap, void *tab, uint64_t cap, unsigned long long *full_flag,
                   void *stream);
 
+// ---- front end at scale, bdeg_rank.cu
+long long rank_modp(const int64_t *A, int n, int m, uint32_t p, int device, void *stream);
+
 }  // namespace bdeg

@@ -330,3 +330,41 @@ def test_emitted_cells_with_normals_are_lower_facets():
             r = w[l] - sum(hi * vi for hi, vi in zip(h, V[l]))
             assert (r == 0) if l in cell else (r > 0)
         assert abs(det_fraction([list(V[c]) for c in cell])) == vol
+
+
+def test_maximum_K_and_empty_ranges():
+    # K = 32 (33 rows: the largest subset size) on a sparse configuration with
+    # small minors; empty and one-candidate rank intervals
+    K = 32
+    V = [tuple(1 if i == j else 0 for j in range(K)) for i in range(K)]
+    V.append(tuple([1] * K))
+    V.append(tuple([1 if j % 3 else -1 for j in range(K)]))
+    V = [(1,) + v[1:] for v in V]
+    w = W.liftings(len(V), 42)
+    o = enumerate_range(K, V, w, threads=8)
+    plan = B.Plan.from_points(V, w)
+    _assert_same(_gpu(plan.degree_range(0, math.comb(len(V), K))), o)
+    for b in (0, 7, math.comb(len(V), K)):
+        r = plan.degree_range(b, b)
+        assert (r.candidates, r.degree, r.cells, r.singular) == (0, 0, 0, 0)
+    for b in (0, 100, math.comb(len(V), K) - 1):
+        _assert_same(_gpu(plan.degree_range(b, b + 1)), enumerate_range(K, V, w, b, b + 1))
+
+
+def test_front_end_at_scale_table2():
+    # GPU row reduction mod primes reproduces Table 2,
+    # dims up to m = k = 40 (n = 4800 variables), and Table 1 entries checked
+    # against the exact SNF of the front end
+    import os
+    want = {}
+    with open(os.path.join(os.path.dirname(__file__), "golden", "table2_dims.txt")) as f:
+        for line in f:
+            if line.strip() and not line.startswith("#"):
+                mm, dd = map(int, line.split())
+                want[mm] = dd
+    for mm in sorted(want):
+        A, b = W.master_space_system(mm, mm)
+        assert B.dimension_modp(A) == want[mm], mm
+    for (m, k) in [(2, 3), (3, 5), (4, 7), (8, 8)]:
+        A, b = W.master_space_system(m, k)
+        assert B.dimension_modp(A) == B.Plan.from_system(A, b).info().dim
