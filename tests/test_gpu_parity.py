@@ -365,6 +365,15 @@ def test_front_end_at_scale_table2():
     for mm in sorted(want):
         A, b = W.master_space_system(mm, mm)
         assert B.dimension_modp(A) == want[mm], mm
+    from oracle import analyze
     for (m, k) in [(2, 3), (3, 5), (4, 7), (8, 8)]:
         A, b = W.master_space_system(m, k)
-        assert B.dimension_modp(A) == B.Plan.from_system(A, b).info().dim
+        assert B.dimension_modp(A) == analyze(A, b)["dim"]
+    rng = W.SplitMix64(9)                     # random full-rank and rank-deficient matrices
+    for _ in range(6):
+        n, m = 3 + rng.uniform_int(0, 20), 2 + rng.uniform_int(0, 20)
+        A = [[rng.uniform_int(-5, 5) for _ in range(m)] for _ in range(n)]
+        if m > 2:
+            for i in range(n):
+                A[i][m - 1] = A[i][0] - 2 * A[i][1]
+        assert B.dimension_modp(A) == analyze(A)["dim"]
