@@ -19,6 +19,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 namespace bdeg {
 namespace walk {
 
@@ -346,6 +348,247 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
             if (st[i]) atomicAdd(a.stats + i, st[i]);
 }
 
+// ------------------------------------------------------------------------
+// Divide-and-conquer leave-one-out elimination (one warp per cell).  A node
+// holds the cell's points [a, b) still to be eliminated, in a row-compacted
+// buffer whose other K - (b - a) cell points are eliminated; its children
+// eliminate one half and recurse into the other.  The K leaves are the K
+// ridges; total pivot steps O(K log K) instead of O(K^2) from scratch.
+// Buffers: rows [0, R-1) are the alive V rows, row R-1 the lift row.
+
+// ridge test on a 2-row state (x = remaining V row, y = lift row); inserts the
+// neighbour across the ridge (cell minus p) into the hash set / next frontier
+template <int NPL>
+__device__ __forceinline__ void ridge_step(const int64_t *bx, const int64_t *by, int64_t g, M128 ridge, int p,
+                                           int N, int lane, const WalkArgs &a, unsigned long long (&st)[6]) {
+    int64_t x[NPL], yk[NPL];
+    bool valid[NPL];
+    const int kappa = g > 0 ? 1 : -1;
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) {
+        const int l = lane + 32 * q;
+        x[q] = bx[l];
+        yk[q] = kappa > 0 ? by[l] : -by[l];
+        valid[q] = l < N && !mbit(ridge, l);
+    }
+    ++st[0];
+    int64_t xps = x[0];
+#pragma unroll
+    for (int q = 1; q < NPL; ++q) if ((p >> 5) == q) xps = x[q];
+    const int64_t xp = __shfl_sync(FULL, (long long)xps, p & 31);
+    if (xp == 0) { ++st[2]; return; }
+    const bool want_pos = xp < 0;                 // the neighbour is on the other side
+    bool bad0 = false;
+    uint32_t kk = 0xFFFFFFFFu;
+    uint32_t key[NPL];
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) {
+        bad0 |= valid[q] && x[q] == 0 && yk[q] < 0;
+        const uint32_t o = ford(__fdividef((float)yk[q], (float)x[q]));
+        key[q] = want_pos ? o : ~o;
+        const bool side = want_pos ? x[q] > 0 : x[q] < 0;
+        if (valid[q] && side) kk = min(kk, key[q]);
+    }
+    if (__any_sync(FULL, bad0)) { ++st[2]; return; }
+    const uint32_t mk = __reduce_min_sync(FULL, kk);
+    if (mk == 0xFFFFFFFFu) { ++st[5]; return; }          // boundary ridge
+    int found = -1;
+    bool tie = false;
+#pragma unroll
+    for (int cq = 0; cq < NPL; ++cq) {
+        const bool side = want_pos ? x[cq] > 0 : x[cq] < 0;
+        uint32_t cand = __ballot_sync(FULL, valid[cq] && side && key[cq] <= mk + 64u);
+        while (cand) {
+            const int j = 32 * cq + __ffs(cand) - 1;
+            cand &= cand - 1;
+            const int64_t xj = __shfl_sync(FULL, (long long)x[cq], j & 31);
+            const int64_t yj = __shfl_sync(FULL, (long long)yk[cq], j & 31);
+            bool bad = false, zero = false;
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int l = lane + 32 * q;
+                if (valid[q] && l != j) {
+                    i128 c = (i128)xj * yk[q] - (i128)x[q] * yj;
+                    if (xj < 0) c = -c;
+                    bad |= c < 0;
+                    zero |= c == 0;
+                }
+            }
+            if (__any_sync(FULL, bad)) continue;
+            if (__any_sync(FULL, zero)) { tie = true; continue; }
+            found = j;
+        }
+    }
+    if (tie) ++st[1];
+    if (found < 0) { if (!tie) ++st[5]; return; }
+    if (lane == 0) {
+        const M128 nm = mset(ridge, found);
+        bool full = false;
+        if (insert(a.table, a.cap, nm, full)) {
+            const unsigned long long pos = atomicAdd(a.next_cnt, 1ull);
+            a.next[pos] = nm;
+        }
+        if (full) ++st[3];
+    }
+}
+
+// eliminate pivot column p in the compact buffer B (R rows x NP); R -= 1
+template <int NPL, bool WIDE>
+__device__ __forceinline__ bool dc_eliminate(int64_t *B, int &R, int p, int64_t &prev, int lane, bool &ovf,
+                                             int64_t limV, int64_t limL) {
+    constexpr int NP = 32 * NPL;
+    const bool nz = lane < R - 1 && B[lane * NP + p] != 0;
+    const unsigned bal = __ballot_sync(FULL, nz);
+    if (bal == 0) return false;
+    const int r = __ffs(bal) - 1;
+    const int64_t piv = B[r * NP + p];
+    const Div dv = make_div(prev);
+    int64_t prow[NPL];
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) prow[q] = B[r * NP + lane + 32 * q];
+    for (int i = 0; i < R; ++i) {
+        if (i == r) continue;
+        const int64_t ci = B[i * NP + p];
+        const int64_t lim = i < R - 1 ? limV : limL;
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const int l = lane + 32 * q;
+            int64_t v;
+            if constexpr (WIDE) {
+                v = qdiv((i128)piv * B[i * NP + l] - (i128)ci * prow[q], dv, ovf);
+            } else {
+                v = qdiv64(piv * B[i * NP + l] - ci * prow[q], dv);
+                ovf |= !inside(v, lim);
+            }
+            B[i * NP + l] = v;
+        }
+    }
+    __syncwarp();
+    // compaction: the last V row takes the pivot row's slot, the lift row moves down
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) {
+        const int l = lane + 32 * q;
+        if (r != R - 2) B[r * NP + l] = B[(R - 2) * NP + l];
+        B[(R - 2) * NP + l] = B[(R - 1) * NP + l];
+    }
+    __syncwarp();
+    --R;
+    prev = piv;
+    return true;
+}
+
+constexpr int kDcDepth = 7;   // K <= 32: ceil(log2 32) + 1 levels
+
+// all K ridges of cell m; returns false on overflow (caller retries WIDE)
+template <int NPL, bool WIDE>
+__device__ bool dc_cell(const int64_t *Lsm, int64_t *bufs, const int *roff, int K, int N, M128 m, int lane,
+                        const WalkArgs &a, unsigned long long (&st)[6], int64_t limV, int64_t limL) {
+    constexpr int NP = 32 * NPL;
+    int pts[32];                      // the cell's points (uniform; small)
+    int na = 0;
+#pragma unroll 1
+    for (int t = 0; t < K; ++t) pts[na++] = mnth(m, t);
+    // depth 0: the full lifted matrix
+    int64_t *B0 = bufs;
+    __syncwarp();
+    for (int i = 0; i <= K; ++i)
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const int l = lane + 32 * q;
+            B0[i * NP + l] = (l < N) ? Lsm[l * (K + 1) + i] : 0;
+        }
+    __syncwarp();
+    int A[kDcDepth], Bn[kDcDepth], stage[kDcDepth], R[kDcDepth];
+    int64_t prev[kDcDepth];
+    int d = 0;
+    A[0] = 0; Bn[0] = K; stage[0] = 0; R[0] = K + 1; prev[0] = 1;
+    bool ovf = false;
+    while (d >= 0) {
+        int64_t *Bd = bufs + (size_t)roff[d] * NP;
+        if (Bn[d] - A[d] == 1) {
+            ridge_step<NPL>(Bd, Bd + NP, prev[d], mclear(m, pts[A[d]]), pts[A[d]], N, lane, a, st);
+            --d;
+            continue;
+        }
+        if (stage[d] == 2) { --d; continue; }
+        const int mid = (A[d] + Bn[d]) / 2;
+        const int e0 = stage[d] == 0 ? mid : A[d];       // eliminate [e0, e1)
+        const int e1 = stage[d] == 0 ? Bn[d] : mid;
+        int64_t *C = bufs + (size_t)roff[d + 1] * NP;
+        __syncwarp();
+        for (int i = 0; i < R[d]; ++i)
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) C[i * NP + lane + 32 * q] = Bd[i * NP + lane + 32 * q];
+        __syncwarp();
+        int Rc = R[d];
+        int64_t pc = prev[d];
+        for (int t = e0; t < e1; ++t) {
+            if (!dc_eliminate<NPL, WIDE>(C, Rc, pts[t], pc, lane, ovf, limV, limL)) { ++st[2]; return true; }
+            if (__any_sync(FULL, ovf)) return false;
+        }
+        A[d + 1] = stage[d] == 0 ? A[d] : mid;
+        Bn[d + 1] = stage[d] == 0 ? mid : Bn[d];
+        stage[d] += 1;
+        ++d;
+        stage[d] = 0;
+        R[d] = Rc;
+        prev[d] = pc;
+    }
+    return true;
+}
+
+template <int NPL>
+__global__ void __launch_bounds__(kWarps * 32) k_walk_dc(WalkArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int K = a.K, N = a.N;
+    int64_t *Lsm = reinterpret_cast<int64_t *>(smem);
+    const int lsz = (K + 1) * N;
+    for (int i = threadIdx.x; i < lsz; i += blockDim.x) Lsm[i] = a.L[i];
+    // row offsets of the per-depth buffers (rows shrink by the eliminated half)
+    int roff[kDcDepth + 1];
+    {
+        int g = K, rows = K + 1, off = 0;
+        for (int d = 0; d <= kDcDepth; ++d) {
+            roff[d] = off;
+            off += rows;
+            rows -= g / 2;
+            g = (g + 1) / 2;
+            if (rows < 2) rows = 2;
+        }
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NP = 32 * NPL;
+    const int rows_total = roff[kDcDepth];
+    int64_t *bufs = reinterpret_cast<int64_t *>(smem + ((lsz * 8 + 15) & ~15)) + (size_t)warp * rows_total * NP;
+    unsigned long long st[6] = {0, 0, 0, 0, 0, 0};
+    for (;;) {
+        unsigned long long idx = 0;
+        if (lane == 0) idx = atomicAdd(a.counter, 1ull);
+        idx = __shfl_sync(FULL, idx, 0);
+        if (idx >= a.ncur) break;
+        const M128 m = a.cur[idx];
+        bool done = false;
+        if (a.limV > 0) done = dc_cell<NPL, false>(Lsm, bufs, roff, K, N, m, lane, a, st, a.limV, a.limL);
+        if (!done && !dc_cell<NPL, true>(Lsm, bufs, roff, K, N, m, lane, a, st, 0, 0)) ++st[4];
+    }
+    if (lane == 0)
+        for (int i = 0; i < 6; ++i)
+            if (st[i]) atomicAdd(a.stats + i, st[i]);
+}
+
+size_t walk_dc_rows(int K) {
+    int g = K, rows = K + 1, off = 0;
+    for (int d = 0; d < kDcDepth; ++d) {
+        off += rows;
+        rows -= g / 2;
+        g = (g + 1) / 2;
+        if (rows < 2) rows = 2;
+    }
+    return (size_t)off;
+}
+
 // |det| of every cell in the table (one warp per cell) into 4 limbs + count
 template <int NPL>
 __global__ void __launch_bounds__(kWarps * 32) k_cellvol(const int64_t *L, int K, int N,
@@ -434,10 +677,20 @@ size_t walk_smem_bytes(int K, int N) {
 
 template <int NPL>
 static int walk_npl(const walk::WalkArgs &a, int grid, size_t smem) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)walk::k_walk<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    const size_t dsmem = (((size_t)(a.K + 1) * a.N * 8 + 15) & ~(size_t)15) +
+                         (size_t)walk::kWarps * walk::walk_dc_rows(a.K) * 32 * NPL * 8;
+    // per-ridge elimination from scratch: A/B reference, and when the D&C buffers exceed smem
+    if (std::getenv("BDEG_WALK_SCRATCH") || dsmem > 227 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute((const void *)walk::k_walk<NPL>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        walk::k_walk<NPL><<<grid, walk::kWarps * 32, smem, (cudaStream_t)a.stream>>>(a);
+        return (int)cudaGetLastError();
+    }
+    cudaError_t e = cudaFuncSetAttribute((const void *)walk::k_walk_dc<NPL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
     if (e != cudaSuccess) return (int)e;
-    walk::k_walk<NPL><<<grid, walk::kWarps * 32, smem, (cudaStream_t)a.stream>>>(a);
+    walk::k_walk_dc<NPL><<<grid, walk::kWarps * 32, dsmem, (cudaStream_t)a.stream>>>(a);
     return (int)cudaGetLastError();
 }
 
