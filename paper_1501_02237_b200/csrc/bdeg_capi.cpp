@@ -609,7 +609,8 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
     DevBuf table, cur, nxt, aux;
     if (!table.alloc(cap * 16) || !cur.alloc(ccap * 16) || !nxt.alloc(ncap * 16) || !aux.alloc(16 * 8))
         return fail(p, BDEG_E_CUDA, "cudaMalloc failed");
-    unsigned long long *next_cnt = aux.u(), *counter = aux.u() + 1, *stats = aux.u() + 2;   // stats: 8 slots
+    // aux: [0] next count, [1] work counter, [2..9] stats, [10..14] level volume limbs + cells
+    unsigned long long *next_cnt = aux.u(), *counter = aux.u() + 1, *stats = aux.u() + 2, *lvol = aux.u() + 10;
     cudaMemsetAsync(table.p, 0, cap * 16, st);
     const uint64_t h0 = walk_hash(start[0], start[1]) & (cap - 1);
     cudaMemcpyAsync((char *)table.p + h0 * 16, start, 16, cudaMemcpyHostToDevice, st);
@@ -619,7 +620,9 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
     // (tier 0: 2^31 / 2^31, tier 1: 2^Bv / 2^Bl); tier 2 plans go wide at once
     const int64_t limV = p->tier == 2 ? 0 : (int64_t)1 << (p->tier == 0 ? 30 : p->bits_v);
     const int64_t limL = p->tier == 2 ? 0 : (int64_t)1 << (p->tier == 0 ? 31 : p->bits_l);
-    uint64_t ridges = 0, boundary = 0;
+    uint64_t ridges = 0, boundary = 0, fused_cells = 0, wide_cells = 0;
+    u128 fused_vol = 0;
+    int fused = 0;
     auto grow_table = [&](uint64_t ncap_t) -> bdeg_status {
         DevBuf t2;
         if (!t2.alloc(ncap_t * 16)) return fail(p, BDEG_E_CUDA, "cudaMalloc (hash set grow) failed");
@@ -633,6 +636,7 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
         return BDEG_OK;
     };
     while (ncur > 0) {
+        const double t_level = now_ms();
         // hash set at load <= 1/2 for the expected growth; re-run on overflow
         if ((total_cells + 3 * ncur) * 2 > cap) {
             bdeg_status s = grow_table(pow2_at_least(3 * (total_cells + 3 * ncur)));
@@ -643,12 +647,12 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
             if (!nxt.alloc(ncap * 16)) return fail(p, BDEG_E_CUDA, "cudaMalloc (frontier) failed");
         }
         cudaMemsetAsync(aux.p, 0, 16 * 8, st);
-        uint64_t h[10];
+        uint64_t h[16];
         for (int attempt = 0;; ++attempt) {
             int rc = launch_walk(p->d_L, K, p->N, cur.p, ncur, nxt.p, next_cnt, table.p, cap, counter, stats,
-                                 grid, st, limV, limL);
+                                 grid, st, limV, limL, lvol, &fused);
             if (rc) return fail(p, BDEG_E_CUDA, std::string("k_walk: ") + cudaGetErrorString((cudaError_t)rc));
-            cudaMemcpyAsync(h, aux.p, 10 * 8, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(h, aux.p, 16 * 8, cudaMemcpyDeviceToHost, st);
             cudaError_t ce = cudaStreamSynchronize(st);
             if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
             if (h[2 + 3] == 0) break;
@@ -656,15 +660,24 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
             if (attempt > 4) return fail(p, BDEG_E_TOO_LARGE, "cell walk: hash set overflow");
             bdeg_status s = grow_table(cap * 4);
             if (s) return s;
-            cudaMemsetAsync(counter, 0, 8, st);
-            cudaMemsetAsync(stats, 0, 8 * 8, st);
+            // redo the level; the cells it already appended stay (the grown table holds them)
+            cudaMemsetAsync(counter, 0, 15 * 8, st);   // work counter, stats, level volumes
         }
         const uint64_t *sv = h + 2;
         ridges += sv[0];
         boundary += sv[5];
+        wide_cells += sv[6];
         if (sv[1] > 0) return fail(p, BDEG_E_DEGENERATE, "degenerate lifting: a ridge has a tie (cell walk)");
         if (sv[2] > 0 || sv[4] > 0)
-            return fail(p, BDEG_E_TOO_LARGE, "cell walk: inconsistent ridge or value overflow");
+            return fail(p, BDEG_E_TOO_LARGE, "cell walk: inconsistent ridge or value overflow (level " +
+                                                 std::to_string(levels) + ": " + std::to_string(sv[2]) +
+                                                 " inconsistent, " + std::to_string(sv[4]) + " overflow)");
+        if (dbg && std::getenv("BDEG_DEBUG_LEVELS"))
+            fprintf(stderr, "  level %d: cells %llu -> %llu, %.2f ms (cap %llu)\n", levels,
+                    (unsigned long long)ncur, (unsigned long long)h[0], now_ms() - t_level,
+                    (unsigned long long)cap);
+        for (int i = 3; i >= 0; --i) fused_vol += (u128)h[10 + i] << (32 * i);
+        fused_cells += h[14];
         std::swap(cur.p, nxt.p);
         std::swap(ccap, ncap);
         ncur = h[0];
@@ -672,9 +685,22 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
         ++levels;
     }
     if (dbg)
-        fprintf(stderr, "[bdeg walk] start cell %.2f ms, %d levels, walk %.2f ms, cells %llu, cap %llu\n",
-                t_start - t0, levels, now_ms() - t_start, (unsigned long long)total_cells,
-                (unsigned long long)cap);
+        fprintf(stderr, "[bdeg walk] start cell %.2f ms, %d levels, walk %.2f ms, cells %llu, cap %llu, "
+                "int128 redo %llu, tier %d\n", t_start - t0, levels, now_ms() - t_start,
+                (unsigned long long)total_cells, (unsigned long long)cap, (unsigned long long)wide_cells, p->tier);
+    if (fused) {   // the D&C walk summed |det| as it went
+        r->deg_lo = (uint64_t)fused_vol;
+        r->deg_hi = (int64_t)(uint64_t)(fused_vol >> 64);
+        r->cells = fused_cells;
+        r->candidates = 0;
+        r->singular = 0;
+        r->singular_complete = 0;
+        r->leaves = ridges;
+        r->dead_leaves = boundary;
+        if (r->cells != total_cells) return fail(p, BDEG_E_TOO_LARGE, "cell walk: table / frontier mismatch");
+        *kms += now_ms() - t0;
+        return BDEG_OK;
+    }
     // exact volumes, one determinant per cell
     cudaMemsetAsync(aux.p, 0, 16 * 8, st);
     int rc = launch_cellvol(p->d_L, K, p->N, table.p, cap, aux.u() + 8, aux.u(), grid, st, limV, limL);

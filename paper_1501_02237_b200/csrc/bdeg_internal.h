@@ -112,7 +112,8 @@ size_t walk_smem_bytes(int K, int N);
 uint64_t walk_hash(uint64_t lo, uint64_t hi);
 int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, void *next,
                 unsigned long long *next_cnt, void *table, uint64_t cap, unsigned long long *counter,
-                unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL);
+                unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL,
+                unsigned long long *vol, int *fused);
 int launch_cellvol(const int64_t *L, int K, int N, const void *table, uint64_t cap, unsigned long long *out,
                    unsigned long long *counter, int grid, void *stream, int64_t limV, int64_t limL);
 int launch_rehash(const void *old, uint64_t oldcap, void *tab, uint64_t cap, unsigned long long *full_flag,

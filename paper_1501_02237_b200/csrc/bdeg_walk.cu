@@ -19,6 +19,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace bdeg {
@@ -218,8 +219,10 @@ struct WalkArgs {
     uint64_t cap;                     // power of two
     unsigned long long *counter;      // work counter
     int64_t limV, limL;               // int64 fast-path bounds (0: always int128)
+    unsigned long long *vol;          // D&C walk: [4 limbs of sum |det|, cells] of this level
     unsigned long long *stats;        // [0] ridges tested, [1] ties, [2] inconsistent,
-                                      // [3] table full, [4] overflow, [5] boundary ridges
+                                      // [3] table full, [4] overflow, [5] boundary ridges,
+                                      // [6] cells redone with int128 numerators (D&C walk)
     int grid;
     void *stream;
 };
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
 // ridge test on a 2-row state (x = remaining V row, y = lift row); inserts the
 // neighbour across the ridge (cell minus p) into the hash set / next frontier
 template <int NPL>
-__device__ __forceinline__ void ridge_step(const int64_t *bx, const int64_t *by, int64_t g, M128 ridge, int p,
+__device__ __forceinline__ int64_t ridge_step(const int64_t *bx, const int64_t *by, int64_t g, M128 ridge, int p,
                                            int N, int lane, const WalkArgs &a, unsigned long long (&st)[6]) {
     int64_t x[NPL], yk[NPL];
     bool valid[NPL];
@@ -376,7 +379,7 @@ __device__ __forceinline__ void ridge_step(const int64_t *bx, const int64_t *by,
 #pragma unroll
     for (int q = 1; q < NPL; ++q) if ((p >> 5) == q) xps = x[q];
     const int64_t xp = __shfl_sync(FULL, (long long)xps, p & 31);
-    if (xp == 0) { ++st[2]; return; }
+    if (xp == 0) { ++st[2]; return 0; }
     const bool want_pos = xp < 0;                 // the neighbour is on the other side
     bool bad0 = false;
     uint32_t kk = 0xFFFFFFFFu;
@@ -389,9 +392,9 @@ __device__ __forceinline__ void ridge_step(const int64_t *bx, const int64_t *by,
         const bool side = want_pos ? x[q] > 0 : x[q] < 0;
         if (valid[q] && side) kk = min(kk, key[q]);
     }
-    if (__any_sync(FULL, bad0)) { ++st[2]; return; }
+    if (__any_sync(FULL, bad0)) { ++st[2]; return xp; }
     const uint32_t mk = __reduce_min_sync(FULL, kk);
-    if (mk == 0xFFFFFFFFu) { ++st[5]; return; }          // boundary ridge
+    if (mk == 0xFFFFFFFFu) { ++st[5]; return xp; }          // boundary ridge
     int found = -1;
     bool tie = false;
 #pragma unroll
@@ -420,7 +423,7 @@ __device__ __forceinline__ void ridge_step(const int64_t *bx, const int64_t *by,
         }
     }
     if (tie) ++st[1];
-    if (found < 0) { if (!tie) ++st[5]; return; }
+    if (found < 0) { if (!tie) ++st[5]; return xp; }
     if (lane == 0) {
         const M128 nm = mset(ridge, found);
         bool full = false;
@@ -430,84 +433,96 @@ __device__ __forceinline__ void ridge_step(const int64_t *bx, const int64_t *by,
         }
         if (full) ++st[3];
     }
+    return xp;
 }
 
-// eliminate pivot column p in the compact buffer B (R rows x NP); R -= 1
+// Eliminate pivot column p: rows of src (R rows, V rows [0, R-1), lift row
+// R-1) -> dst with R-1 rows, row-compacted (the last V row takes the pivot
+// row's slot, the lift row moves down one).  src == dst is allowed: each lane
+// touches only its own columns, column p's multipliers are read up front and
+// rows are visited in increasing order.  Column p is written too (it becomes
+// exactly 0): stale values there would feed later steps' inexact divisions
+// and raise false overflow flags.  R <= 32.
 template <int NPL, bool WIDE>
-__device__ __forceinline__ bool dc_eliminate(int64_t *B, int &R, int p, int64_t &prev, int lane, bool &ovf,
-                                             int64_t limV, int64_t limL) {
+__device__ __forceinline__ bool dc_eliminate(const int64_t *src, int64_t *dst, int &R, int p, int64_t &prev,
+                                             int lane, bool &ovf, int64_t limV, int64_t limL) {
     constexpr int NP = 32 * NPL;
-    const bool nz = lane < R - 1 && B[lane * NP + p] != 0;
-    const unsigned bal = __ballot_sync(FULL, nz);
+    __syncwarp();
+    const int64_t cl = lane < R ? src[lane * NP + p] : 0;
+    const unsigned bal = __ballot_sync(FULL, lane < R - 1 && cl != 0);
     if (bal == 0) return false;
     const int r = __ffs(bal) - 1;
-    const int64_t piv = B[r * NP + p];
+    const int64_t piv = __shfl_sync(FULL, (long long)cl, r);
     const Div dv = make_div(prev);
     int64_t prow[NPL];
 #pragma unroll
-    for (int q = 0; q < NPL; ++q) prow[q] = B[r * NP + lane + 32 * q];
+    for (int q = 0; q < NPL; ++q) prow[q] = src[r * NP + lane + 32 * q];
+    __syncwarp();   // every lane has read column p before its owner rewrites it
     for (int i = 0; i < R; ++i) {
         if (i == r) continue;
-        const int64_t ci = B[i * NP + p];
+        const int64_t ci = __shfl_sync(FULL, (long long)cl, i);
         const int64_t lim = i < R - 1 ? limV : limL;
-        __syncwarp();
+        const int o = i == R - 1 ? R - 2 : (i == R - 2 ? r : i);
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
             const int l = lane + 32 * q;
             int64_t v;
             if constexpr (WIDE) {
-                v = qdiv((i128)piv * B[i * NP + l] - (i128)ci * prow[q], dv, ovf);
+                v = qdiv((i128)piv * src[i * NP + l] - (i128)ci * prow[q], dv, ovf);
             } else {
-                v = qdiv64(piv * B[i * NP + l] - ci * prow[q], dv);
+                v = qdiv64(piv * src[i * NP + l] - ci * prow[q], dv);
                 ovf |= !inside(v, lim);
             }
-            B[i * NP + l] = v;
+            dst[o * NP + l] = v;
         }
     }
-    __syncwarp();
-    // compaction: the last V row takes the pivot row's slot, the lift row moves down
-#pragma unroll
-    for (int q = 0; q < NPL; ++q) {
-        const int l = lane + 32 * q;
-        if (r != R - 2) B[r * NP + l] = B[(R - 2) * NP + l];
-        B[(R - 2) * NP + l] = B[(R - 1) * NP + l];
-    }
-    __syncwarp();
     --R;
     prev = piv;
     return true;
 }
 
-constexpr int kDcDepth = 7;   // K <= 32: ceil(log2 32) + 1 levels
+constexpr int kDcDepth = 7;   // K <= 31: ceil(log2 31) + 1 levels
 
-// all K ridges of cell m; returns false on overflow (caller retries WIDE)
+// per-depth row offsets (depth >= 1; depth 0 is the shared L) and their total
+__host__ __device__ inline int dc_offsets(int K, int *roff) {
+    int g = K, rows = K + 1, off = 0;
+    for (int d = 0; d <= kDcDepth; ++d) {
+        if (roff) roff[d] = off;
+        if (d > 0) off += rows;
+        rows -= g / 2;
+        g = (g + 1) / 2;
+        if (rows < 2) rows = 2;
+    }
+    return off;
+}
+
+// All K ridges of cell m; false on int64 overflow (the caller retries WIDE).
+// vol = |det| of the cell (the pivot x_p of the first leaf).  Lsm: row-major
+// (K+1) x NP lifted matrix = the depth-0 buffer.
 template <int NPL, bool WIDE>
 __device__ bool dc_cell(const int64_t *Lsm, int64_t *bufs, const int *roff, int K, int N, M128 m, int lane,
-                        const WalkArgs &a, unsigned long long (&st)[6], int64_t limV, int64_t limL) {
+                        const WalkArgs &a, unsigned long long (&st)[6], int64_t limV, int64_t limL,
+                        uint64_t &vol) {
     constexpr int NP = 32 * NPL;
-    int pts[32];                      // the cell's points (uniform; small)
-    int na = 0;
-#pragma unroll 1
-    for (int t = 0; t < K; ++t) pts[na++] = mnth(m, t);
-    // depth 0: the full lifted matrix
-    int64_t *B0 = bufs;
-    __syncwarp();
-    for (int i = 0; i <= K; ++i)
-#pragma unroll
-        for (int q = 0; q < NPL; ++q) {
-            const int l = lane + 32 * q;
-            B0[i * NP + l] = (l < N) ? Lsm[l * (K + 1) + i] : 0;
-        }
-    __syncwarp();
+    int pts[32];                      // the cell's points, ascending
+    {
+        int n = 0;
+        uint64_t w = m.lo;
+        while (w) { pts[n++] = __ffsll((long long)w) - 1; w &= w - 1; }
+        w = m.hi;
+        while (w) { pts[n++] = 64 + __ffsll((long long)w) - 1; w &= w - 1; }
+    }
     int A[kDcDepth], Bn[kDcDepth], stage[kDcDepth], R[kDcDepth];
     int64_t prev[kDcDepth];
     int d = 0;
     A[0] = 0; Bn[0] = K; stage[0] = 0; R[0] = K + 1; prev[0] = 1;
     bool ovf = false;
+    vol = 0;
     while (d >= 0) {
-        int64_t *Bd = bufs + (size_t)roff[d] * NP;
+        const int64_t *Bd = d == 0 ? Lsm : bufs + (size_t)roff[d] * NP;
         if (Bn[d] - A[d] == 1) {
-            ridge_step<NPL>(Bd, Bd + NP, prev[d], mclear(m, pts[A[d]]), pts[A[d]], N, lane, a, st);
+            const int64_t xp = ridge_step<NPL>(Bd, Bd + NP, prev[d], mclear(m, pts[A[d]]), pts[A[d]], N, lane, a, st);
+            if (A[d] == 0) vol = (uint64_t)(xp < 0 ? -xp : xp);
             --d;
             continue;
         }
@@ -516,15 +531,13 @@ __device__ bool dc_cell(const int64_t *Lsm, int64_t *bufs, const int *roff, int 
         const int e0 = stage[d] == 0 ? mid : A[d];       // eliminate [e0, e1)
         const int e1 = stage[d] == 0 ? Bn[d] : mid;
         int64_t *C = bufs + (size_t)roff[d + 1] * NP;
-        __syncwarp();
-        for (int i = 0; i < R[d]; ++i)
-#pragma unroll
-            for (int q = 0; q < NPL; ++q) C[i * NP + lane + 32 * q] = Bd[i * NP + lane + 32 * q];
-        __syncwarp();
         int Rc = R[d];
         int64_t pc = prev[d];
         for (int t = e0; t < e1; ++t) {
-            if (!dc_eliminate<NPL, WIDE>(C, Rc, pts[t], pc, lane, ovf, limV, limL)) { ++st[2]; return true; }
+            if (!dc_eliminate<NPL, WIDE>(t == e0 ? Bd : C, C, Rc, pts[t], pc, lane, ovf, limV, limL)) {
+                ++st[2];
+                return true;
+            }
             if (__any_sync(FULL, ovf)) return false;
         }
         A[d + 1] = stage[d] == 0 ? A[d] : mid;
@@ -538,55 +551,55 @@ __device__ bool dc_cell(const int64_t *Lsm, int64_t *bufs, const int *roff, int 
     return true;
 }
 
+// One warp per cell of the frontier (walk level); also sums |det| and counts
+// the level's cells (each cell is in exactly one frontier).
 template <int NPL>
-__global__ void __launch_bounds__(kWarps * 32) k_walk_dc(WalkArgs a) {
+__global__ void __launch_bounds__(512) k_walk_dc(WalkArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NP = 32 * NPL;
     const int K = a.K, N = a.N;
-    int64_t *Lsm = reinterpret_cast<int64_t *>(smem);
-    const int lsz = (K + 1) * N;
-    for (int i = threadIdx.x; i < lsz; i += blockDim.x) Lsm[i] = a.L[i];
-    // row offsets of the per-depth buffers (rows shrink by the eliminated half)
-    int roff[kDcDepth + 1];
-    {
-        int g = K, rows = K + 1, off = 0;
-        for (int d = 0; d <= kDcDepth; ++d) {
-            roff[d] = off;
-            off += rows;
-            rows -= g / 2;
-            g = (g + 1) / 2;
-            if (rows < 2) rows = 2;
-        }
+    int64_t *Lsm = reinterpret_cast<int64_t *>(smem);               // row-major (K+1) x NP
+    for (int t = threadIdx.x; t < (K + 1) * NP; t += blockDim.x) {
+        const int i = t / NP, l = t - i * NP;
+        Lsm[t] = l < N ? a.L[(size_t)l * (K + 1) + i] : 0;
     }
+    int roff[kDcDepth + 1];
+    const int rows_total = dc_offsets(K, roff);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int NP = 32 * NPL;
-    const int rows_total = roff[kDcDepth];
-    int64_t *bufs = reinterpret_cast<int64_t *>(smem + ((lsz * 8 + 15) & ~15)) + (size_t)warp * rows_total * NP;
+    // roff[d] for d >= 1 counts from roff[1] = 0
+    int64_t *bufs = Lsm + (size_t)(K + 1) * NP + (size_t)warp * rows_total * NP;
     unsigned long long st[6] = {0, 0, 0, 0, 0, 0};
+    uint64_t lo = 0, hi = 0, cells = 0, fallbacks = 0;
     for (;;) {
         unsigned long long idx = 0;
         if (lane == 0) idx = atomicAdd(a.counter, 1ull);
         idx = __shfl_sync(FULL, idx, 0);
         if (idx >= a.ncur) break;
         const M128 m = a.cur[idx];
+        uint64_t v = 0;
         bool done = false;
-        if (a.limV > 0) done = dc_cell<NPL, false>(Lsm, bufs, roff, K, N, m, lane, a, st, a.limV, a.limL);
-        if (!done && !dc_cell<NPL, true>(Lsm, bufs, roff, K, N, m, lane, a, st, 0, 0)) ++st[4];
+        if (a.limV > 0) done = dc_cell<NPL, false>(Lsm, bufs, roff, K, N, m, lane, a, st, a.limV, a.limL, v);
+        fallbacks += !done;
+        if (!done && !dc_cell<NPL, true>(Lsm, bufs, roff, K, N, m, lane, a, st, 0, 0, v)) {
+            ++st[4];
+            continue;
+        }
+        const uint64_t t = lo + v;
+        hi += t < lo;
+        lo = t;
+        ++cells;
     }
-    if (lane == 0)
+    if (lane == 0) {
         for (int i = 0; i < 6; ++i)
             if (st[i]) atomicAdd(a.stats + i, st[i]);
-}
-
-size_t walk_dc_rows(int K) {
-    int g = K, rows = K + 1, off = 0;
-    for (int d = 0; d < kDcDepth; ++d) {
-        off += rows;
-        rows -= g / 2;
-        g = (g + 1) / 2;
-        if (rows < 2) rows = 2;
+        atomicAdd(a.vol + 0, lo & 0xFFFFFFFFull);
+        atomicAdd(a.vol + 1, lo >> 32);
+        atomicAdd(a.vol + 2, hi & 0xFFFFFFFFull);
+        atomicAdd(a.vol + 3, hi >> 32);
+        atomicAdd(a.vol + 4, cells);
+        if (fallbacks) atomicAdd(a.stats + 6, fallbacks);   // cells redone in int128
     }
-    return (size_t)off;
 }
 
 // |det| of every cell in the table (one warp per cell) into 4 limbs + count
@@ -675,29 +688,42 @@ size_t walk_smem_bytes(int K, int N) {
     return (((size_t)(K + 1) * N * 8 + 15) & ~(size_t)15) + (size_t)walk::kWarps * (K + 1) * 32 * npl_of(N) * 8;
 }
 
+// D&C walk kernel when it fits (K <= 31, >= 2 warps' buffers in shared
+// memory); *fused = 1 then (the launch also summed the level's volumes).
 template <int NPL>
-static int walk_npl(const walk::WalkArgs &a, int grid, size_t smem) {
-    const size_t dsmem = (((size_t)(a.K + 1) * a.N * 8 + 15) & ~(size_t)15) +
-                         (size_t)walk::kWarps * walk::walk_dc_rows(a.K) * 32 * NPL * 8;
-    // per-ridge elimination from scratch: A/B reference, and when the D&C buffers exceed smem
-    if (std::getenv("BDEG_WALK_SCRATCH") || dsmem > 227 * 1024) {
+static int walk_npl(const walk::WalkArgs &a, int grid, size_t smem, int *fused) {
+    const size_t lbytes = (size_t)(a.K + 1) * 32 * NPL * 8;
+    const size_t per_warp = (size_t)walk::dc_offsets(a.K, nullptr) * 32 * NPL * 8;
+    const size_t budget = 227 * 1024;
+    const int nw = lbytes + per_warp > budget ? 0 : (int)std::min<size_t>(16, (budget - lbytes) / per_warp);
+    *fused = 0;
+    // per-ridge elimination from scratch: A/B reference, K > 31, or buffers beyond smem
+    if (std::getenv("BDEG_WALK_SCRATCH") || a.K > 31 || nw < 2) {
         cudaError_t e = cudaFuncSetAttribute((const void *)walk::k_walk<NPL>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
         walk::k_walk<NPL><<<grid, walk::kWarps * 32, smem, (cudaStream_t)a.stream>>>(a);
         return (int)cudaGetLastError();
     }
+    const size_t dsmem = lbytes + (size_t)nw * per_warp;
     cudaError_t e = cudaFuncSetAttribute((const void *)walk::k_walk_dc<NPL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
     if (e != cudaSuccess) return (int)e;
-    walk::k_walk_dc<NPL><<<grid, walk::kWarps * 32, dsmem, (cudaStream_t)a.stream>>>(a);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = std::max<int>(1, (int)((228 * 1024) / (dsmem + 1024)));
+    walk::k_walk_dc<NPL><<<sms * per_sm, nw * 32, dsmem, (cudaStream_t)a.stream>>>(a);
+    *fused = 1;
     return (int)cudaGetLastError();
 }
 
 int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, void *next,
                 unsigned long long *next_cnt, void *table, uint64_t cap, unsigned long long *counter,
-                unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL) {
+                unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL,
+                unsigned long long *vol, int *fused) {
     walk::WalkArgs a;
+    a.vol = vol;
     a.limV = limV;
     a.limL = limL;
     a.L = L; a.K = K; a.N = N; a.cur = (const walk::M128 *)cur; a.ncur = ncur; a.next = (walk::M128 *)next;
@@ -706,10 +732,10 @@ int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, 
     const size_t smem = walk_smem_bytes(K, N);
     int rc;
     switch (npl_of(N)) {
-        case 1: rc = walk_npl<1>(a, grid, smem); break;
-        case 2: rc = walk_npl<2>(a, grid, smem); break;
-        case 3: rc = walk_npl<3>(a, grid, smem); break;
-        default: rc = walk_npl<4>(a, grid, smem); break;
+        case 1: rc = walk_npl<1>(a, grid, smem, fused); break;
+        case 2: rc = walk_npl<2>(a, grid, smem, fused); break;
+        case 3: rc = walk_npl<3>(a, grid, smem, fused); break;
+        default: rc = walk_npl<4>(a, grid, smem, fused); break;
     }
     launch_counter_add(1);
     return rc;
