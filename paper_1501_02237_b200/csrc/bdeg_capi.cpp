@@ -606,12 +606,14 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
     const int K = p->K;
     int levels = 0;
     uint64_t cap = 1ull << 20, ncur = 1, total_cells = 1, ccap = 1 << 16, ncap = 1 << 16;
-    DevBuf table, cur, nxt, aux;
-    if (!table.alloc(cap * 16) || !cur.alloc(ccap * 16) || !nxt.alloc(ncap * 16) || !aux.alloc(16 * 8))
+    DevBuf table, tags, cur, nxt, aux;
+    if (!table.alloc(cap * 16) || !tags.alloc(cap) || !cur.alloc(ccap * 16) || !nxt.alloc(ncap * 16) ||
+        !aux.alloc(16 * 8))
         return fail(p, BDEG_E_CUDA, "cudaMalloc failed");
     // aux: [0] next count, [1] work counter, [2..9] stats, [10..14] level volume limbs + cells
     unsigned long long *next_cnt = aux.u(), *counter = aux.u() + 1, *stats = aux.u() + 2, *lvol = aux.u() + 10;
     cudaMemsetAsync(table.p, 0, cap * 16, st);
+    cudaMemsetAsync(tags.p, 0, cap, st);                 // level 0 (the start cell) has tag 0
     const uint64_t h0 = walk_hash(start[0], start[1]) & (cap - 1);
     cudaMemcpyAsync((char *)table.p + h0 * 16, start, 16, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(cur.p, start, 16, cudaMemcpyHostToDevice, st);
@@ -620,47 +622,76 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
     // (tier 0: 2^31 / 2^31, tier 1: 2^Bv / 2^Bl); tier 2 plans go wide at once
     const int64_t limV = p->tier == 2 ? 0 : (int64_t)1 << (p->tier == 0 ? 30 : p->bits_v);
     const int64_t limL = p->tier == 2 ? 0 : (int64_t)1 << (p->tier == 0 ? 31 : p->bits_l);
-    uint64_t ridges = 0, boundary = 0, fused_cells = 0, wide_cells = 0;
+    uint64_t ridges = 0, boundary = 0, fused_cells = 0, wide_cells = 0, collects = 0;
     u128 fused_vol = 0;
     int fused = 0;
+    double growth = K;                                   // expected next / current frontier size
+    const bool tight = std::getenv("BDEG_WALK_TIGHT") != nullptr;
+    if (tight) growth = 0;
     auto grow_table = [&](uint64_t ncap_t) -> bdeg_status {
-        DevBuf t2;
-        if (!t2.alloc(ncap_t * 16)) return fail(p, BDEG_E_CUDA, "cudaMalloc (hash set grow) failed");
+        DevBuf t2, g2;
+        if (!t2.alloc(ncap_t * 16) || !g2.alloc(ncap_t))
+            return fail(p, BDEG_E_TOO_LARGE, "cell walk: hash set of " + std::to_string(ncap_t) +
+                                                 " slots does not fit in device memory");
         cudaMemsetAsync(t2.p, 0, ncap_t * 16, st);
+        cudaMemsetAsync(g2.p, 0, ncap_t, st);
         cudaMemsetAsync(stats, 0, 8 * 8, st);
-        int rc = launch_rehash(table.p, cap, t2.p, ncap_t, stats + 3, st);
+        int rc = launch_rehash(table.p, (const uint8_t *)tags.p, cap, t2.p, (uint8_t *)g2.p, ncap_t, stats + 3, st);
         if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
         cudaStreamSynchronize(st);
         std::swap(table.p, t2.p);
+        std::swap(tags.p, g2.p);
         cap = ncap_t;
         return BDEG_OK;
     };
+    // the largest power-of-two table (17 B per slot) that fits beside `keep` bytes
+    auto mem_cap = [&](uint64_t keep) -> uint64_t {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const uint64_t avail = fr > keep + (2ull << 30) ? fr - keep - (2ull << 30) : 0;
+        uint64_t c = 1;
+        while (c * 2 * 17 <= avail) c <<= 1;
+        return c;
+    };
     while (ncur > 0) {
         const double t_level = now_ms();
-        // hash set at load <= 1/2 for the expected growth; re-run on overflow
-        if ((total_cells + 3 * ncur) * 2 > cap) {
-            bdeg_status s = grow_table(pow2_at_least(3 * (total_cells + 3 * ncur)));
-            if (s) return s;
+        const uint64_t est = std::min<uint64_t>(ncur * (uint64_t)K, (uint64_t)(ncur * growth) + (tight ? 1 : 1024));
+        // hash set at load <= 1/2 for the expected growth (<= 3/4 when device
+        // memory is the limit); a level that overflows it is re-run
+        const uint64_t need = total_cells + est;
+        if (need * 2 > cap) {
+            uint64_t want = pow2_at_least(3 * need);
+            const uint64_t lim = std::max(cap, mem_cap((ccap + 2 * est) * 16));   // old table is still live
+            if (want > lim) want = lim;
+            if (want > cap) {
+                bdeg_status s = grow_table(want);
+                if (s) return s;
+            }
+            if (need * 4 > cap * 3)
+                return fail(p, BDEG_E_TOO_LARGE, "cell walk: " + std::to_string(need) +
+                                                     " cells exceed the hash set that fits in device memory");
         }
-        if (ncur * K > ncap) {                     // next frontier: <= ncur * K cells
-            ncap = pow2_at_least(ncur * K);
-            if (!nxt.alloc(ncap * 16)) return fail(p, BDEG_E_CUDA, "cudaMalloc (frontier) failed");
+        if (est > ncap) {                          // next frontier (collected from the table if it overflows)
+            ncap = pow2_at_least(est);
+            if (!nxt.alloc(ncap * 16)) return fail(p, BDEG_E_TOO_LARGE, "cudaMalloc (frontier) failed");
         }
+        const unsigned tag = (unsigned)(levels + 1) & 255u;
         cudaMemsetAsync(aux.p, 0, 16 * 8, st);
         uint64_t h[16];
         for (int attempt = 0;; ++attempt) {
             int rc = launch_walk(p->d_L, K, p->N, cur.p, ncur, nxt.p, next_cnt, table.p, cap, counter, stats,
-                                 grid, st, limV, limL, lvol, &fused);
+                                 grid, st, limV, limL, lvol, &fused, (uint8_t *)tags.p, tag, ncap);
             if (rc) return fail(p, BDEG_E_CUDA, std::string("k_walk: ") + cudaGetErrorString((cudaError_t)rc));
             cudaMemcpyAsync(h, aux.p, 16 * 8, cudaMemcpyDeviceToHost, st);
             cudaError_t ce = cudaStreamSynchronize(st);
             if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
             if (h[2 + 3] == 0) break;
-            // full: keep the cells already appended, grow, redo the level
+            // full: keep the cells already inserted (tagged), grow, redo the level
             if (attempt > 4) return fail(p, BDEG_E_TOO_LARGE, "cell walk: hash set overflow");
-            bdeg_status s = grow_table(cap * 4);
+            const uint64_t want = std::min(cap * 2, std::max(cap, mem_cap((ccap + ncap) * 16)));
+            if (want <= cap) return fail(p, BDEG_E_TOO_LARGE, "cell walk: hash set full at the device memory limit");
+            bdeg_status s = grow_table(want);
             if (s) return s;
-            // redo the level; the cells it already appended stay (the grown table holds them)
             cudaMemsetAsync(counter, 0, 15 * 8, st);   // work counter, stats, level volumes
         }
         const uint64_t *sv = h + 2;
@@ -672,22 +703,45 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
             return fail(p, BDEG_E_TOO_LARGE, "cell walk: inconsistent ridge or value overflow (level " +
                                                  std::to_string(levels) + ": " + std::to_string(sv[2]) +
                                                  " inconsistent, " + std::to_string(sv[4]) + " overflow)");
+        const uint64_t nnext = h[0];
+        if (nnext > ncap) {
+            // frontier overflow: the level's cells are all in the table with
+            // this tag; collect them into a buffer of the right size
+            ncap = pow2_at_least(nnext);
+            if (!nxt.alloc(ncap * 16)) return fail(p, BDEG_E_TOO_LARGE, "cudaMalloc (frontier) failed");
+            cudaMemsetAsync(next_cnt, 0, 8, st);
+            int rc = launch_collect(table.p, (const uint8_t *)tags.p, cap, (uint8_t)tag, nxt.p, next_cnt, st);
+            if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
+            uint64_t got = 0;
+            cudaMemcpyAsync(&got, next_cnt, 8, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            // levels more than 255 apart share a tag: only cells of this level
+            // can carry it while fewer than 256 levels exist
+            if (got != nnext && levels < 255)
+                return fail(p, BDEG_E_TOO_LARGE, "cell walk: frontier re-collection mismatch");
+            if (got != nnext) return fail(p, BDEG_E_TOO_LARGE, "cell walk: > 255 levels with frontier overflow");
+            ++collects;
+        }
         if (dbg && std::getenv("BDEG_DEBUG_LEVELS"))
-            fprintf(stderr, "  level %d: cells %llu -> %llu, %.2f ms (cap %llu)\n", levels,
-                    (unsigned long long)ncur, (unsigned long long)h[0], now_ms() - t_level,
-                    (unsigned long long)cap);
+            fprintf(stderr, "  level %d: cells %llu -> %llu, %.2f ms (cap %llu, next cap %llu)\n", levels,
+                    (unsigned long long)ncur, (unsigned long long)nnext, now_ms() - t_level,
+                    (unsigned long long)cap, (unsigned long long)ncap);
         for (int i = 3; i >= 0; --i) fused_vol += (u128)h[10 + i] << (32 * i);
         fused_cells += h[14];
+        // growth estimate for the next level: the ratio just seen, with slack
+        growth = std::min<double>(K, 1.25 * (double)nnext / (double)ncur + 0.25);
+        if (tight) growth = 0;                     // test knob: every growing level overflows
         std::swap(cur.p, nxt.p);
         std::swap(ccap, ncap);
-        ncur = h[0];
+        ncur = nnext;
         total_cells += ncur;
         ++levels;
     }
     if (dbg)
         fprintf(stderr, "[bdeg walk] start cell %.2f ms, %d levels, walk %.2f ms, cells %llu, cap %llu, "
-                "int128 redo %llu, tier %d\n", t_start - t0, levels, now_ms() - t_start,
-                (unsigned long long)total_cells, (unsigned long long)cap, (unsigned long long)wide_cells, p->tier);
+                "int128 redo %llu, tier %d, frontier re-collections %llu\n", t_start - t0, levels,
+                now_ms() - t_start, (unsigned long long)total_cells, (unsigned long long)cap,
+                (unsigned long long)wide_cells, p->tier, (unsigned long long)collects);
     if (fused) {   // the D&C walk summed |det| as it went
         r->deg_lo = (uint64_t)fused_vol;
         r->deg_hi = (int64_t)(uint64_t)(fused_vol >> 64);

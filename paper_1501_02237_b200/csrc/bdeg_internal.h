@@ -113,11 +113,13 @@ uint64_t walk_hash(uint64_t lo, uint64_t hi);
 int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, void *next,
                 unsigned long long *next_cnt, void *table, uint64_t cap, unsigned long long *counter,
                 unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL,
-                unsigned long long *vol, int *fused);
+                unsigned long long *vol, int *fused, uint8_t *tags, unsigned tag, uint64_t next_cap);
 int launch_cellvol(const int64_t *L, int K, int N, const void *table, uint64_t cap, unsigned long long *out,
                    unsigned long long *counter, int grid, void *stream, int64_t limV, int64_t limL);
-int launch_rehash(const void *old, uint64_t oldcap, void *tab, uint64_t cap, unsigned long long *full_flag,
-                  void *stream);
+int launch_rehash(const void *old, const uint8_t *old_tags, uint64_t oldcap, void *tab, uint8_t *tags, uint64_t cap,
+                  unsigned long long *full_flag, void *stream);
+int launch_collect(const void *tab, const uint8_t *tags, uint64_t cap, uint8_t tag, void *out,
+                   unsigned long long *cnt, void *stream);
 
 // ---- front end at scale, bdeg_rank.cu
 long long rank_modp(const int64_t *A, int n, int m, uint32_t p, int device, void *stream);

@@ -217,6 +217,9 @@ struct WalkArgs {
     unsigned long long *next_cnt;
     M128 *table;                      // hash set of cell masks ({0,0} = empty)
     uint64_t cap;                     // power of two
+    uint8_t *tags;                    // per-slot level tag (mod 256)
+    uint8_t tag;                      // tag of the next level's cells
+    uint64_t next_cap;                // capacity of `next`
     unsigned long long *counter;      // work counter
     int64_t limV, limL;               // int64 fast-path bounds (0: always int128)
     unsigned long long *vol;          // D&C walk: [4 limbs of sum |det|, cells] of this level
@@ -227,13 +230,20 @@ struct WalkArgs {
     void *stream;
 };
 
-__device__ __forceinline__ bool insert(M128 *table, uint64_t cap, M128 key, bool &full) {
+// Insert key (linear probing); true if it was new.  tags (optional): the
+// slot's walk level (mod 256) is recorded beside it, so a level's cells can be
+// re-collected from the table (frontier overflow).
+__device__ __forceinline__ bool insert(M128 *table, uint64_t cap, M128 key, bool &full,
+                                       uint8_t *tags = nullptr, uint8_t tag = 0) {
     uint64_t h = mhash(key) & (cap - 1);
     const M128 empty = {0, 0};
-    const uint64_t max_probe = cap < 4096 ? cap : 4096;   // load <= 1/2: short probes
+    const uint64_t max_probe = cap < 4096 ? cap : 4096;   // load <= 3/4: short probes
     for (uint64_t probe = 0; probe < max_probe; ++probe) {
         const M128 old = cas128(table + h, empty, key);
-        if (old.lo == 0 && old.hi == 0) return true;
+        if (old.lo == 0 && old.hi == 0) {
+            if (tags) tags[h] = tag;
+            return true;
+        }
         if (old.lo == key.lo && old.hi == key.hi) return false;
         h = (h + 1) & (cap - 1);
     }
@@ -339,9 +349,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
         if (lane == 0) {
             const M128 nm = mset(ridge, found);
             bool full = false;
-            if (insert(a.table, a.cap, nm, full)) {
+            if (insert(a.table, a.cap, nm, full, a.tags, a.tag)) {
                 const unsigned long long pos = atomicAdd(a.next_cnt, 1ull);
-                a.next[pos] = nm;
+                if (pos < a.next_cap) a.next[pos] = nm;   // else re-collected by tag
             }
             if (full) ++st[3];
         }
@@ -427,9 +437,9 @@ __device__ __forceinline__ int64_t ridge_step(const int64_t *bx, const int64_t *
     if (lane == 0) {
         const M128 nm = mset(ridge, found);
         bool full = false;
-        if (insert(a.table, a.cap, nm, full)) {
+        if (insert(a.table, a.cap, nm, full, a.tags, a.tag)) {
             const unsigned long long pos = atomicAdd(a.next_cnt, 1ull);
-            a.next[pos] = nm;
+            if (pos < a.next_cap) a.next[pos] = nm;   // else re-collected by tag
         }
         if (full) ++st[3];
     }
@@ -653,14 +663,25 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellvol(const int64_t *L, int K
     }
 }
 
-__global__ void k_rehash(const M128 *old, uint64_t oldcap, M128 *tab, uint64_t cap,
-                         unsigned long long *full_flag) {
+__global__ void k_rehash(const M128 *old, const uint8_t *old_tags, uint64_t oldcap, M128 *tab, uint8_t *tags,
+                         uint64_t cap, unsigned long long *full_flag) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < oldcap; i += (uint64_t)gridDim.x * blockDim.x) {
         const M128 k = old[i];
         if (k.lo == 0 && k.hi == 0) continue;
         bool full = false;
-        insert(tab, cap, k, full);
+        insert(tab, cap, k, full, tags, old_tags[i]);
         if (full) atomicAdd(full_flag, 1ull);
+    }
+}
+
+// the cells of one level (by tag) into out[0, *cnt)
+__global__ void k_collect(const M128 *tab, const uint8_t *tags, uint64_t cap, uint8_t tag, M128 *out,
+                          unsigned long long *cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (tags[i] != tag) continue;
+        const M128 k = tab[i];
+        if (k.lo == 0 && k.hi == 0) continue;
+        out[atomicAdd(cnt, 1ull)] = k;
     }
 }
 
@@ -674,10 +695,18 @@ static uint64_t hmix(uint64_t z) {
 }
 uint64_t walk_hash(uint64_t lo, uint64_t hi) { return hmix(lo ^ hmix(hi + 0x9E3779B97F4A7C15ull)); }
 
-int launch_rehash(const void *old, uint64_t oldcap, void *tab, uint64_t cap, unsigned long long *full_flag,
-                  void *stream) {
-    walk::k_rehash<<<1184, 256, 0, (cudaStream_t)stream>>>((const walk::M128 *)old, oldcap, (walk::M128 *)tab, cap,
-                                                           full_flag);
+int launch_rehash(const void *old, const uint8_t *old_tags, uint64_t oldcap, void *tab, uint8_t *tags, uint64_t cap,
+                  unsigned long long *full_flag, void *stream) {
+    walk::k_rehash<<<1184, 256, 0, (cudaStream_t)stream>>>((const walk::M128 *)old, old_tags, oldcap,
+                                                           (walk::M128 *)tab, tags, cap, full_flag);
+    launch_counter_add(1);
+    return (int)cudaGetLastError();
+}
+
+int launch_collect(const void *tab, const uint8_t *tags, uint64_t cap, uint8_t tag, void *out,
+                   unsigned long long *cnt, void *stream) {
+    walk::k_collect<<<1184, 256, 0, (cudaStream_t)stream>>>((const walk::M128 *)tab, tags, cap, tag,
+                                                            (walk::M128 *)out, cnt);
     launch_counter_add(1);
     return (int)cudaGetLastError();
 }
@@ -721,9 +750,12 @@ static int walk_npl(const walk::WalkArgs &a, int grid, size_t smem, int *fused) 
 int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, void *next,
                 unsigned long long *next_cnt, void *table, uint64_t cap, unsigned long long *counter,
                 unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL,
-                unsigned long long *vol, int *fused) {
+                unsigned long long *vol, int *fused, uint8_t *tags, unsigned tag, uint64_t next_cap) {
     walk::WalkArgs a;
     a.vol = vol;
+    a.tags = tags;
+    a.tag = (uint8_t)tag;
+    a.next_cap = next_cap;
     a.limV = limV;
     a.limL = limL;
     a.L = L; a.K = K; a.N = N; a.cur = (const walk::M128 *)cur; a.ncur = ncur; a.next = (walk::M128 *)next;

@@ -283,6 +283,18 @@ def test_walk_matches_enumeration(name):
     assert (r.degree, r.cells) == (o["volume"], o["cells"])
 
 
+def test_walk_frontier_recollection(monkeypatch):
+    # a frontier buffer too small for every growing level: the level's cells
+    # are re-collected from the hash set by their level tag (same answer)
+    V, w = W.c5_points(2, n_points=36, dim=5)
+    base = B.Plan.from_points(V, w).degree_walk()
+    monkeypatch.setenv("BDEG_WALK_TIGHT", "1")
+    r = B.Plan.from_points(V, w).degree_walk()
+    assert (r.degree, r.cells) == (base.degree, base.cells)
+    o = enumerate_range(6, V, w, threads=8)
+    assert (r.degree, r.cells) == (o["volume"], o["cells"])
+
+
 def test_walk_points_and_c2():
     for (V, w, K) in [(W.c5_points(1, n_points=14, dim=4) + (5,)),
                       (W.c5_points(2, n_points=36, dim=5) + (6,)),
