@@ -303,7 +303,7 @@ def run_gpu(args):
             "time_to_degree_ms": e2e_step,
             "result": {"degree": res.degree, "cells": res.cells, "singular": res.singular,
                        "candidates": res.candidates, "ties": res.ties,
-                       "overflow_reruns": res.overflow_reruns},
+                       "overflow_reruns": res.overflow_reruns, "leaves": res.leaves},
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
                          "unit": "Tintop/s", "frac": achieved / peak_ops, "traffic": traffic,
                          "peak_basis": f"128 int lane-ops/clk/SM x {n_sm} SMs x {sm_mhz:.0f} MHz "

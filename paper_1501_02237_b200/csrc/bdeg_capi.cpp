@@ -606,6 +606,8 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
     const int K = p->K;
     int levels = 0;
     uint64_t cap = 1ull << 20, ncur = 1, total_cells = 1, ccap = 1 << 16, ncap = 1 << 16;
+    if (const char *c0 = std::getenv("BDEG_WALK_CAP0"))   // test knob: initial hash set slots
+        cap = pow2_at_least(std::max<uint64_t>(64, std::strtoull(c0, nullptr, 10)));
     DevBuf table, tags, cur, nxt, aux;
     if (!table.alloc(cap * 16) || !tags.alloc(cap) || !cur.alloc(ccap * 16) || !nxt.alloc(ncap * 16) ||
         !aux.alloc(16 * 8))
@@ -628,7 +630,15 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
     double growth = K;                                   // expected next / current frontier size
     const bool tight = std::getenv("BDEG_WALK_TIGHT") != nullptr;
     if (tight) growth = 0;
-    auto grow_table = [&](uint64_t ncap_t) -> bdeg_status {
+    // Breadth-first window (fused D&C walk only; the separate volume pass
+    // needs every cell): the table must hold levels L-1, L, L+1 while level
+    // L is expanded, so older levels are dropped whenever the table is
+    // rebuilt.  lsz[l] = cells of level l; live = cells in the table.
+    std::vector<uint64_t> lsz{1};
+    uint64_t live = 1, evictions = 0;
+    int oldest = 0;                                      // oldest level possibly in the table
+    // keep_from >= 0: keep only levels keep_from .. keep_from+2
+    auto grow_table = [&](uint64_t ncap_t, int keep_from = -1) -> bdeg_status {
         DevBuf t2, g2;
         if (!t2.alloc(ncap_t * 16) || !g2.alloc(ncap_t))
             return fail(p, BDEG_E_TOO_LARGE, "cell walk: hash set of " + std::to_string(ncap_t) +
@@ -636,7 +646,12 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
         cudaMemsetAsync(t2.p, 0, ncap_t * 16, st);
         cudaMemsetAsync(g2.p, 0, ncap_t, st);
         cudaMemsetAsync(stats, 0, 8 * 8, st);
-        int rc = launch_rehash(table.p, (const uint8_t *)tags.p, cap, t2.p, (uint8_t *)g2.p, ncap_t, stats + 3, st);
+        int rc = launch_rehash(table.p, (const uint8_t *)tags.p, cap, t2.p, (uint8_t *)g2.p, ncap_t, stats + 3, st,
+                               (uint8_t)(keep_from & 255), keep_from >= 0 ? 3 : 0);
+        if (keep_from >= 0) {
+            oldest = keep_from;
+            ++evictions;
+        }
         if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
         cudaStreamSynchronize(st);
         std::swap(table.p, t2.p);
@@ -658,7 +673,19 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
         const uint64_t est = std::min<uint64_t>(ncur * (uint64_t)K, (uint64_t)(ncur * growth) + (tight ? 1 : 1024));
         // hash set at load <= 1/2 for the expected growth (<= 3/4 when device
         // memory is the limit); a level that overflows it is re-run
-        const uint64_t need = total_cells + est;
+        const int L = levels;
+        const uint64_t window = (L > 0 ? lsz[L - 1] : 0) + lsz[L];
+        // evict when the table is due to grow (or the level tags would wrap)
+        const bool evictable = fused && L >= 2 && oldest < L - 1;
+        if (evictable && (L - oldest >= 250 || (live + est) * 2 > cap)) {
+            const uint64_t lim = std::max<uint64_t>(1024, mem_cap((ccap + 2 * est) * 16));
+            uint64_t want = std::min(pow2_at_least(3 * (window + est)), lim);
+            while (want * 3 < window * 4 + 4 && want < lim) want <<= 1;
+            bdeg_status s = grow_table(std::max<uint64_t>(want, 1024), L - 1);
+            if (s) return s;
+            live = window;
+        }
+        const uint64_t need = live + est;
         if (need * 2 > cap) {
             uint64_t want = pow2_at_least(3 * need);
             const uint64_t lim = std::max(cap, mem_cap((ccap + 2 * est) * 16));   // old table is still live
@@ -688,10 +715,19 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
             if (h[2 + 3] == 0) break;
             // full: keep the cells already inserted (tagged), grow, redo the level
             if (attempt > 4) return fail(p, BDEG_E_TOO_LARGE, "cell walk: hash set overflow");
-            const uint64_t want = std::min(cap * 2, std::max(cap, mem_cap((ccap + ncap) * 16)));
-            if (want <= cap) return fail(p, BDEG_E_TOO_LARGE, "cell walk: hash set full at the device memory limit");
-            bdeg_status s = grow_table(want);
-            if (s) return s;
+            if (fused && L >= 2 && oldest < L - 1) {     // drop levels < L-1 (and grow if it helps)
+                const uint64_t keep = window + h[0];
+                const uint64_t lim = std::max<uint64_t>(1024, mem_cap((ccap + ncap) * 16));
+                uint64_t want = std::min(std::max(cap, pow2_at_least(3 * keep)), lim);
+                bdeg_status s = grow_table(want, L - 1);
+                if (s) return s;
+                live = keep;
+            } else {
+                const uint64_t want = std::min(cap * 2, std::max(cap, mem_cap((ccap + ncap) * 16)));
+                if (want <= cap) return fail(p, BDEG_E_TOO_LARGE, "cell walk: hash set full at the device memory limit");
+                bdeg_status s = grow_table(want);
+                if (s) return s;
+            }
             cudaMemsetAsync(counter, 0, 15 * 8, st);   // work counter, stats, level volumes
         }
         const uint64_t *sv = h + 2;
@@ -717,7 +753,7 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
             cudaStreamSynchronize(st);
             // levels more than 255 apart share a tag: only cells of this level
             // can carry it while fewer than 256 levels exist
-            if (got != nnext && levels < 255)
+            if (got != nnext && levels - oldest < 255)
                 return fail(p, BDEG_E_TOO_LARGE, "cell walk: frontier re-collection mismatch");
             if (got != nnext) return fail(p, BDEG_E_TOO_LARGE, "cell walk: > 255 levels with frontier overflow");
             ++collects;
@@ -735,13 +771,16 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
         std::swap(ccap, ncap);
         ncur = nnext;
         total_cells += ncur;
+        live += ncur;
+        lsz.push_back(ncur);
         ++levels;
     }
     if (dbg)
         fprintf(stderr, "[bdeg walk] start cell %.2f ms, %d levels, walk %.2f ms, cells %llu, cap %llu, "
-                "int128 redo %llu, tier %d, frontier re-collections %llu\n", t_start - t0, levels,
-                now_ms() - t_start, (unsigned long long)total_cells, (unsigned long long)cap,
-                (unsigned long long)wide_cells, p->tier, (unsigned long long)collects);
+                "int128 redo %llu, tier %d, frontier re-collections %llu, window evictions %llu\n", t_start - t0,
+                levels, now_ms() - t_start, (unsigned long long)total_cells, (unsigned long long)cap,
+                (unsigned long long)wide_cells, p->tier, (unsigned long long)collects,
+                (unsigned long long)evictions);
     if (fused) {   // the D&C walk summed |det| as it went
         r->deg_lo = (uint64_t)fused_vol;
         r->deg_hi = (int64_t)(uint64_t)(fused_vol >> 64);

@@ -117,7 +117,7 @@ int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, 
 int launch_cellvol(const int64_t *L, int K, int N, const void *table, uint64_t cap, unsigned long long *out,
                    unsigned long long *counter, int grid, void *stream, int64_t limV, int64_t limL);
 int launch_rehash(const void *old, const uint8_t *old_tags, uint64_t oldcap, void *tab, uint8_t *tags, uint64_t cap,
-                  unsigned long long *full_flag, void *stream);
+                  unsigned long long *full_flag, void *stream, uint8_t keep0 = 0, int keep_n = 0);
 int launch_collect(const void *tab, const uint8_t *tags, uint64_t cap, uint8_t tag, void *out,
                    unsigned long long *cnt, void *stream);
 

@@ -663,11 +663,18 @@ __global__ void __launch_bounds__(kWarps * 32) k_cellvol(const int64_t *L, int K
     }
 }
 
+// Re-insert the cells of `old` into `tab`.  keep_n > 0: only the cells of
+// the keep_n consecutive levels starting at tag keep0 (mod 256) survive —
+// the breadth-first window: a neighbour of a level-L cell lies in level
+// L-1, L or L+1 (BFS distances of adjacent cells differ by <= 1), so older
+// levels are never looked up again (the paper's hash table
+// P:1134-1162 keeps every face).
 __global__ void k_rehash(const M128 *old, const uint8_t *old_tags, uint64_t oldcap, M128 *tab, uint8_t *tags,
-                         uint64_t cap, unsigned long long *full_flag) {
+                         uint64_t cap, unsigned long long *full_flag, uint8_t keep0, int keep_n) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < oldcap; i += (uint64_t)gridDim.x * blockDim.x) {
         const M128 k = old[i];
         if (k.lo == 0 && k.hi == 0) continue;
+        if (keep_n > 0 && (uint8_t)(old_tags[i] - keep0) >= (unsigned)keep_n) continue;
         bool full = false;
         insert(tab, cap, k, full, tags, old_tags[i]);
         if (full) atomicAdd(full_flag, 1ull);
@@ -696,9 +703,9 @@ static uint64_t hmix(uint64_t z) {
 uint64_t walk_hash(uint64_t lo, uint64_t hi) { return hmix(lo ^ hmix(hi + 0x9E3779B97F4A7C15ull)); }
 
 int launch_rehash(const void *old, const uint8_t *old_tags, uint64_t oldcap, void *tab, uint8_t *tags, uint64_t cap,
-                  unsigned long long *full_flag, void *stream) {
+                  unsigned long long *full_flag, void *stream, uint8_t keep0, int keep_n) {
     walk::k_rehash<<<1184, 256, 0, (cudaStream_t)stream>>>((const walk::M128 *)old, old_tags, oldcap,
-                                                           (walk::M128 *)tab, tags, cap, full_flag);
+                                                           (walk::M128 *)tab, tags, cap, full_flag, keep0, keep_n);
     launch_counter_add(1);
     return (int)cudaGetLastError();
 }

@@ -295,6 +295,26 @@ def test_walk_frontier_recollection(monkeypatch):
     assert (r.degree, r.cells) == (o["volume"], o["cells"])
 
 
+def test_walk_window_eviction(monkeypatch, capfd):
+    # a hash set far too small for the subdivision: levels older than L-1 are
+    # dropped whenever it is rebuilt (BFS window), same degree and cells
+    V, w = W.c5_points(2, n_points=36, dim=5)
+    base = B.Plan.from_points(V, w).degree_walk()
+    monkeypatch.setenv("BDEG_WALK_CAP0", "64")
+    monkeypatch.setenv("BDEG_DEBUG", "1")
+    r = B.Plan.from_points(V, w).degree_walk()
+    err = capfd.readouterr().err
+    assert (r.degree, r.cells) == (base.degree, base.cells)
+    ev = int(err.split("window evictions ")[1].split()[0])
+    assert ev >= 2, err
+    monkeypatch.setenv("BDEG_WALK_TIGHT", "1")     # and with frontier re-collection on top
+    r = B.Plan.from_points(V, w).degree_walk()
+    assert (r.degree, r.cells) == (base.degree, base.cells)
+    A, b = W.master_space_system(3, 3)
+    r = B.Plan.from_system(A, b, seed=1).degree_walk()
+    assert r.degree == 1620
+
+
 def test_walk_points_and_c2():
     for (V, w, K) in [(W.c5_points(1, n_points=14, dim=4) + (5,)),
                       (W.c5_points(2, n_points=36, dim=5) + (6,)),
@@ -389,3 +409,4 @@ def test_front_end_at_scale_table2():
             for i in range(n):
                 A[i][m - 1] = A[i][0] - 2 * A[i][1]
         assert B.dimension_modp(A) == analyze(A)["dim"]
+

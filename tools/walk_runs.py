@@ -18,7 +18,7 @@ for wl in sys.argv[1].split(","):
     if wl.startswith("w"):   # the binomial system itself, generated lifting (basis-seeded if N > 64)
         import workloads as W
         A, b = W.master_space_system(int(wl[1]), int(wl[2]))
-        p = B.Plan.from_system(A, b, seed=1)
+        p = B.Plan.from_system(A, b, seed=int(os.environ.get("WALK_SEED", "1")))
         K, nv = p.info().K, p.info().N
     else:
         p = B.Plan.from_points(V, w)
@@ -26,7 +26,7 @@ for wl in sys.argv[1].split(","):
     t0 = time.perf_counter()
     r = p.degree_walk()
     dt = time.perf_counter() - t0
-    print(json.dumps({"wl": wl, "K": K, "N": nv, "candidates": math.comb(nv, K), "walk_s": dt,
+    print(json.dumps({"wl": wl, "seed": int(os.environ.get("WALK_SEED", "1")), "K": K, "N": nv, "candidates": math.comb(nv, K), "walk_s": dt,
                       "kernel_ms": r.kernel_ms, "degree": r.degree, "cells": r.cells,
                       "ridge_tests": r.leaves, "boundary_ridges": r.dead_leaves,
                       "simplices_per_s": math.comb(nv, K) / dt}), flush=True)
