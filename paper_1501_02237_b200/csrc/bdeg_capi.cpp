@@ -616,7 +616,7 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
     unsigned long long *next_cnt = aux.u(), *counter = aux.u() + 1, *stats = aux.u() + 2, *lvol = aux.u() + 10;
     cudaMemsetAsync(table.p, 0, cap * 16, st);
     cudaMemsetAsync(tags.p, 0, cap, st);                 // level 0 (the start cell) has tag 0
-    const uint64_t h0 = walk_hash(start[0], start[1]) & (cap - 1);
+    const uint64_t h0 = (uint64_t)(((u128)walk_hash(start[0], start[1]) * cap) >> 64);   // = device range reduction
     cudaMemcpyAsync((char *)table.p + h0 * 16, start, 16, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(cur.p, start, 16, cudaMemcpyHostToDevice, st);
     const int grid = std::max(1, dev_info(p->opt.device).sms) * 4;
@@ -624,7 +624,11 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
     // (tier 0: 2^31 / 2^31, tier 1: 2^Bv / 2^Bl); tier 2 plans go wide at once
     const int64_t limV = p->tier == 2 ? 0 : (int64_t)1 << (p->tier == 0 ? 30 : p->bits_v);
     const int64_t limL = p->tier == 2 ? 0 : (int64_t)1 << (p->tier == 0 ? 31 : p->bits_l);
-    uint64_t ridges = 0, boundary = 0, fused_cells = 0, wide_cells = 0, collects = 0;
+    uint64_t ridges = 0, boundary = 0, fused_cells = 0, wide_cells = 0, collects = 0, narrow_redo = 0;
+    // int32-storage D&C walk for tier-0 plans (values < 2^30, lifts < 2^31)
+    const int narrow = (p->tier == 0 && !std::getenv("BDEG_WALK_WIDE")) ? 1 : 0;
+    DevBuf ovfl;
+    uint64_t ovfl_cap = 0;
     u128 fused_vol = 0;
     int fused = 0;
     double growth = K;                                   // expected next / current frontier size
@@ -659,15 +663,14 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
         cap = ncap_t;
         return BDEG_OK;
     };
-    // the largest power-of-two table (17 B per slot) that fits beside `keep` bytes
+    // the largest table (17 B per slot, a multiple of 1024 slots) that fits beside `keep` bytes
     auto mem_cap = [&](uint64_t keep) -> uint64_t {
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
         const uint64_t avail = fr > keep + (2ull << 30) ? fr - keep - (2ull << 30) : 0;
-        uint64_t c = 1;
-        while (c * 2 * 17 <= avail) c <<= 1;
-        return c;
+        return std::max<uint64_t>(1024, (uint64_t)((avail / 17) & ~1023ull));
     };
+    auto round_up = [](uint64_t x) -> uint64_t { return (x + 1023) & ~1023ull; };
     while (ncur > 0) {
         const double t_level = now_ms();
         const uint64_t est = std::min<uint64_t>(ncur * (uint64_t)K, (uint64_t)(ncur * growth) + (tight ? 1 : 1024));
@@ -678,17 +681,42 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
         // evict when the table is due to grow (or the level tags would wrap)
         const bool evictable = fused && L >= 2 && oldest < L - 1;
         if (evictable && (L - oldest >= 250 || (live + est) * 2 > cap)) {
-            const uint64_t lim = std::max<uint64_t>(1024, mem_cap((ccap + 2 * est) * 16));
-            uint64_t want = std::min(pow2_at_least(3 * (window + est)), lim);
-            while (want * 3 < window * 4 + 4 && want < lim) want <<= 1;
-            bdeg_status s = grow_table(std::max<uint64_t>(want, 1024), L - 1);
-            if (s) return s;
+            // rebuild from the frontier buffers: level L is `cur`, level L-1 is
+            // still in `nxt` (the previous `cur`), so the old table is dropped
+            // first and the new one can take all free memory
+            cudaStreamSynchronize(st);
+            table.alloc(0);
+            tags.alloc(0);
+            // (free memory already excludes cur and nxt; keep room for a larger nxt)
+            const uint64_t lim = mem_cap(est > ncap ? round_up(est + est / 8) * 16 : 0);
+            const uint64_t want = std::min(std::max<uint64_t>(round_up(3 * (window + est)), 1024), lim);
+            if (want * 3 < window * 4)
+                return fail(p, BDEG_E_TOO_LARGE, "cell walk: " + std::to_string(window) +
+                                                     " cells of two levels exceed the hash set that fits in device memory");
+            if (!table.alloc(want * 16) || !tags.alloc(want))
+                return fail(p, BDEG_E_TOO_LARGE, "cell walk: cudaMalloc of the hash set failed");
+            cap = want;
+            cudaMemsetAsync(table.p, 0, cap * 16, st);
+            cudaMemsetAsync(tags.p, 0, cap, st);
+            cudaMemsetAsync(stats, 0, 8 * 8, st);
+            int rc = launch_insert_list(nxt.p, lsz[L - 1], table.p, (uint8_t *)tags.p, cap, (uint8_t)((L - 1) & 255),
+                                        stats + 3, st);
+            if (!rc) rc = launch_insert_list(cur.p, ncur, table.p, (uint8_t *)tags.p, cap, (uint8_t)(L & 255),
+                                             stats + 3, st);
+            if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
+            uint64_t fullc = 0;
+            cudaMemcpyAsync(&fullc, stats + 3, 8, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            if (fullc) return fail(p, BDEG_E_TOO_LARGE, "cell walk: window rebuild overflowed the hash set");
+            oldest = L - 1;
+            ++evictions;
             live = window;
         }
         const uint64_t need = live + est;
         if (need * 2 > cap) {
-            uint64_t want = pow2_at_least(3 * need);
-            const uint64_t lim = std::max(cap, mem_cap((ccap + 2 * est) * 16));   // old table is still live
+            uint64_t want = round_up(3 * need);
+            // old table still live (already excluded from free memory); room for a larger nxt
+            const uint64_t lim = std::max(cap, mem_cap(est > ncap ? round_up(est + est / 8) * 16 : 0));
             if (want > lim) want = lim;
             if (want > cap) {
                 bdeg_status s = grow_table(want);
@@ -699,31 +727,53 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
                                                      " cells exceed the hash set that fits in device memory");
         }
         if (est > ncap) {                          // next frontier (collected from the table if it overflows)
-            ncap = pow2_at_least(est);
+            ncap = round_up(est + est / 8);
             if (!nxt.alloc(ncap * 16)) return fail(p, BDEG_E_TOO_LARGE, "cudaMalloc (frontier) failed");
         }
         const unsigned tag = (unsigned)(levels + 1) & 255u;
         cudaMemsetAsync(aux.p, 0, 16 * 8, st);
         uint64_t h[16];
         for (int attempt = 0;; ++attempt) {
+            const uint64_t ocap = std::min<uint64_t>(ncur, 1ull << 20);
+            if (narrow && ocap > ovfl_cap) {
+                ovfl_cap = pow2_at_least(ocap);
+                if (!ovfl.alloc(ovfl_cap * 16)) return fail(p, BDEG_E_CUDA, "cudaMalloc (walk overflow list) failed");
+            }
             int rc = launch_walk(p->d_L, K, p->N, cur.p, ncur, nxt.p, next_cnt, table.p, cap, counter, stats,
-                                 grid, st, limV, limL, lvol, &fused, (uint8_t *)tags.p, tag, ncap);
+                                 grid, st, limV, limL, lvol, &fused, (uint8_t *)tags.p, tag, ncap,
+                                 narrow, ovfl.p, aux.u() + 15, ovfl_cap);
             if (rc) return fail(p, BDEG_E_CUDA, std::string("k_walk: ") + cudaGetErrorString((cudaError_t)rc));
             cudaMemcpyAsync(h, aux.p, 16 * 8, cudaMemcpyDeviceToHost, st);
             cudaError_t ce = cudaStreamSynchronize(st);
             if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+            if (narrow && h[15] > 0) {
+                // cells whose values left int32: redo them with int64 storage (their
+                // volumes were not counted; neighbours they inserted are exact)
+                const bool listed = h[15] <= ovfl_cap;
+                if (listed) cudaMemsetAsync(counter, 0, 8, st);
+                else cudaMemsetAsync(counter, 0, 15 * 8, st);   // list overflow: redo the whole level wide
+                cudaMemsetAsync(aux.u() + 15, 0, 8, st);
+                rc = launch_walk(p->d_L, K, p->N, listed ? ovfl.p : cur.p, listed ? h[15] : ncur, nxt.p, next_cnt,
+                                 table.p, cap, counter, stats, grid, st, limV, limL, lvol, &fused,
+                                 (uint8_t *)tags.p, tag, ncap, 0, nullptr, nullptr, 0);
+                if (rc) return fail(p, BDEG_E_CUDA, std::string("k_walk: ") + cudaGetErrorString((cudaError_t)rc));
+                narrow_redo += listed ? h[15] : ncur;
+                cudaMemcpyAsync(h, aux.p, 16 * 8, cudaMemcpyDeviceToHost, st);
+                ce = cudaStreamSynchronize(st);
+                if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+            }
             if (h[2 + 3] == 0) break;
             // full: keep the cells already inserted (tagged), grow, redo the level
             if (attempt > 4) return fail(p, BDEG_E_TOO_LARGE, "cell walk: hash set overflow");
             if (fused && L >= 2 && oldest < L - 1) {     // drop levels < L-1 (and grow if it helps)
                 const uint64_t keep = window + h[0];
-                const uint64_t lim = std::max<uint64_t>(1024, mem_cap((ccap + ncap) * 16));
-                uint64_t want = std::min(std::max(cap, pow2_at_least(3 * keep)), lim);
+                const uint64_t lim = mem_cap(0);
+                uint64_t want = std::min(std::max(cap, round_up(3 * keep)), lim);
                 bdeg_status s = grow_table(want, L - 1);
                 if (s) return s;
                 live = keep;
             } else {
-                const uint64_t want = std::min(cap * 2, std::max(cap, mem_cap((ccap + ncap) * 16)));
+                const uint64_t want = std::min(cap * 2, std::max(cap, mem_cap(0)));
                 if (want <= cap) return fail(p, BDEG_E_TOO_LARGE, "cell walk: hash set full at the device memory limit");
                 bdeg_status s = grow_table(want);
                 if (s) return s;
@@ -743,7 +793,7 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
         if (nnext > ncap) {
             // frontier overflow: the level's cells are all in the table with
             // this tag; collect them into a buffer of the right size
-            ncap = pow2_at_least(nnext);
+            ncap = round_up(nnext);
             if (!nxt.alloc(ncap * 16)) return fail(p, BDEG_E_TOO_LARGE, "cudaMalloc (frontier) failed");
             cudaMemsetAsync(next_cnt, 0, 8, st);
             int rc = launch_collect(table.p, (const uint8_t *)tags.p, cap, (uint8_t)tag, nxt.p, next_cnt, st);
@@ -765,7 +815,7 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
         for (int i = 3; i >= 0; --i) fused_vol += (u128)h[10 + i] << (32 * i);
         fused_cells += h[14];
         // growth estimate for the next level: the ratio just seen, with slack
-        growth = std::min<double>(K, 1.25 * (double)nnext / (double)ncur + 0.25);
+        growth = std::min<double>(K, 1.1 * (double)nnext / (double)ncur + 0.1);
         if (tight) growth = 0;                     // test knob: every growing level overflows
         std::swap(cur.p, nxt.p);
         std::swap(ccap, ncap);
@@ -777,10 +827,11 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
     }
     if (dbg)
         fprintf(stderr, "[bdeg walk] start cell %.2f ms, %d levels, walk %.2f ms, cells %llu, cap %llu, "
-                "int128 redo %llu, tier %d, frontier re-collections %llu, window evictions %llu\n", t_start - t0,
+                "int128 redo %llu, tier %d, frontier re-collections %llu, window evictions %llu, narrow %d "
+                "(int64 redo %llu)\n", t_start - t0,
                 levels, now_ms() - t_start, (unsigned long long)total_cells, (unsigned long long)cap,
                 (unsigned long long)wide_cells, p->tier, (unsigned long long)collects,
-                (unsigned long long)evictions);
+                (unsigned long long)evictions, narrow, (unsigned long long)narrow_redo);
     if (fused) {   // the D&C walk summed |det| as it went
         r->deg_lo = (uint64_t)fused_vol;
         r->deg_hi = (int64_t)(uint64_t)(fused_vol >> 64);

@@ -113,11 +113,15 @@ uint64_t walk_hash(uint64_t lo, uint64_t hi);
 int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, void *next,
                 unsigned long long *next_cnt, void *table, uint64_t cap, unsigned long long *counter,
                 unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL,
-                unsigned long long *vol, int *fused, uint8_t *tags, unsigned tag, uint64_t next_cap);
+                unsigned long long *vol, int *fused, uint8_t *tags, unsigned tag, uint64_t next_cap,
+                int narrow = 0, void *ovfl = nullptr, unsigned long long *ovfl_cnt = nullptr,
+                uint64_t ovfl_cap = 0);
 int launch_cellvol(const int64_t *L, int K, int N, const void *table, uint64_t cap, unsigned long long *out,
                    unsigned long long *counter, int grid, void *stream, int64_t limV, int64_t limL);
 int launch_rehash(const void *old, const uint8_t *old_tags, uint64_t oldcap, void *tab, uint8_t *tags, uint64_t cap,
                   unsigned long long *full_flag, void *stream, uint8_t keep0 = 0, int keep_n = 0);
+int launch_insert_list(const void *list, uint64_t n, void *tab, uint8_t *tags, uint64_t cap, uint8_t tag,
+                       unsigned long long *full_flag, void *stream);
 int launch_collect(const void *tab, const uint8_t *tags, uint64_t cap, uint8_t tag, void *out,
                    unsigned long long *cnt, void *stream);
 

@@ -104,6 +104,16 @@ __device__ __forceinline__ int32_t qdiv32(int64_t num, const Div &dv, bool &ovf)
 __device__ __forceinline__ bool inside(int64_t v, int64_t lim) {
     return (uint64_t)(v + (lim - 1)) <= (uint64_t)(2 * (lim - 1));
 }
+// |num| < b  (b >= 1)
+__device__ __forceinline__ bool within(int64_t num, int64_t b) {
+    return (uint64_t)(num + (b - 1)) <= (uint64_t)(2 * (b - 1));
+}
+// Exact quotient whose range was established from the numerator (|num| <
+// L * |d| implies |q| < L): no multiply-back is needed.
+__device__ __forceinline__ int32_t qdiv32u(int64_t num, const Div &dv) {
+    if (dv.unit != 0) return (int32_t)(dv.unit > 0 ? num : -num);
+    return (int32_t)((uint32_t)(num >> dv.tz) * (uint32_t)dv.inv);
+}
 __device__ __forceinline__ int64_t qdiv128(i128 num, const Div &dv, bool &ovf) {
     int64_t q;
     if (dv.unit != 0) {
@@ -314,7 +324,7 @@ __device__ __forceinline__ void elim_step(const typename Tr<TIER>::VV (&sv)[NPL]
                                           const typename Tr<TIER>::VL (&sl)[NPL],
                                           const typename Tr<TIER>::VV (&cv)[RV],
                                           typename Tr<TIER>::VL cl, int pr, typename Tr<TIER>::VV piv,
-                                          const Div &dv, const Ctx &cx,
+                                          const Div &dv, int64_t bV, int64_t bL, const Ctx &cx,
                                           typename Tr<TIER>::VV (&ov)[NPL][RV - 1],
                                           typename Tr<TIER>::VL (&ol)[NPL], bool &ovf) {
     typedef typename Tr<TIER>::VV VV;
@@ -330,22 +340,23 @@ __device__ __forceinline__ void elim_step(const typename Tr<TIER>::VV (&sv)[NPL]
             const VV cs = (o < pr) ? cv[o] : cv[o + 1];
             if constexpr (TIER == 2) {
                 ov[q][o] = qdiv128((i128)piv * s - (i128)cs * prow, dv, ovf);
-            } else if constexpr (TIER == 0) {
-                ov[q][o] = qdiv32(madw(piv, s, mulw(-cs, prow)), dv, ovf);
             } else {
-                const int32_t v = qdiv32(madw(piv, s, mulw(-cs, prow)), dv, ovf);
-                ovf |= !inside(v, cx.limV);
-                ov[q][o] = v;
+                // |num| < bV = L |prev|  <=>  |quotient| < L (tier bound)
+                const int64_t num = madw(piv, s, mulw(-cs, prow));
+                ovf |= !within(num, bV);
+                ov[q][o] = qdiv32u(num, dv);
             }
         }
         if constexpr (TIER == 2) {
             ol[q] = qdiv128((i128)piv * sl[q] - (i128)cl * prow, dv, ovf);
         } else if constexpr (TIER == 0) {
-            ol[q] = qdiv32(madw(piv, sl[q], mulw(-cl, prow)), dv, ovf);
+            const int64_t num = madw(piv, sl[q], mulw(-cl, prow));
+            ovf |= !within(num, bL);
+            ol[q] = qdiv32u(num, dv);
         } else {
-            const int64_t v = qdiv64((int64_t)piv * (int64_t)sl[q] - (int64_t)cl * (int64_t)prow, dv);
-            ovf |= !inside(v, cx.limL);
-            ol[q] = (VL)v;
+            const int64_t num = (int64_t)piv * (int64_t)sl[q] - (int64_t)cl * (int64_t)prow;
+            ovf |= !within(num, bL);
+            ol[q] = (VL)qdiv64(num, dv);
         }
     }
 }
@@ -553,7 +564,13 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
         return;
     }
     Div dv;
+    int64_t bV = 0, bL = 0;   // numerator bounds: tier bound x |prev| (tiers 0/1)
     if constexpr (RV > 2 || TIER == 2) dv = make_div(prev);
+    if constexpr (TIER != 2) {
+        const int64_t ap = prev < 0 ? -prev : prev;
+        bV = (TIER == 0 ? (int64_t)INT32_MAX : cx.limV) * ap;
+        bL = (TIER == 0 ? (int64_t)INT32_MAX : cx.limL) * ap;
+    }
     for (int c = lo; c < hi; ++c) {
         const uint64_t nb = base + cx.C(c, i + 1);
         const uint64_t ns = cx.C(c, i);
@@ -594,7 +611,7 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
             VL ol[NPL];
             // overflow is voted once per item (the item is discarded and replayed);
             // loops are index-bounded, so garbage values cannot hang the warp
-            elim_step<TIER, NPL, RV>(sv, sl, cv, cl, pr, piv, dv, cx, ov, ol, ovf);
+            elim_step<TIER, NPL, RV>(sv, sl, cv, cl, pr, piv, dv, bV, bL, cx, ov, ol, ovf);
             const uint64_t cinP = inP | (1ull << c);
             const bool cdead = cx.deg_only && (dead || node_dead<TIER, NPL, RV - 1>(ov, ol, cinP, (int64_t)piv, cx));
             if (cdead && cx.deg_only) {          // no cell in the subtree: skip it
@@ -689,15 +706,28 @@ __device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, co
             const int64_t piv = scr[r * NP + p];
             const Div dv = make_div(prev);
             bool o = false;
+            // tiers 0/1: every value obeys the tier bound (|V| < LV, |lift| < LL,
+            // checked), so numerators are exact in int64 and |num| < L |prev|
+            // <=> |quotient| < L; tier 2: int128 numerators, quotients verified
+            const int64_t ap = prev < 0 ? -prev : prev;
+            const int64_t bV = (TIER == 0 ? (int64_t)INT32_MAX : cx.limV) * ap;
+            const int64_t bL = (TIER == 0 ? (int64_t)INT32_MAX : cx.limL) * ap;
             for (int i = 0; i <= K; ++i) {
                 if (i == r || (i < K && !((alive >> i) & 1ull))) continue;
                 const int64_t ci = scr[i * NP + p];
+                const int64_t b = i < K ? bV : bL;
 #pragma unroll
                 for (int q = 0; q < NPL; ++q) {
                     const int l = lane + 32 * q;
                     if (l == p) continue;
-                    const i128 num = (i128)piv * scr[i * NP + l] - (i128)ci * scr[r * NP + l];
-                    scr[i * NP + l] = qdiv128(num, dv, o);
+                    if constexpr (TIER == 2) {
+                        const i128 num = (i128)piv * scr[i * NP + l] - (i128)ci * scr[r * NP + l];
+                        scr[i * NP + l] = qdiv128(num, dv, o);
+                    } else {
+                        const int64_t num = piv * scr[i * NP + l] - ci * scr[r * NP + l];
+                        o |= !within(num, b);
+                        scr[i * NP + l] = qdiv64(num, dv);
+                    }
                 }
             }
             acc.updates += (uint64_t)(K - t) * N;

@@ -132,6 +132,11 @@ __device__ __forceinline__ int64_t qdiv64(int64_t num, const Div &dv) {
 __device__ __forceinline__ bool inside(int64_t v, int64_t lim) {
     return (uint64_t)(v + (lim - 1)) <= (uint64_t)(2 * (lim - 1));
 }
+// exact quotient known (from |num| < L |d|) to satisfy |q| < L <= 2^31
+__device__ __forceinline__ int32_t qdiv32u(int64_t num, const Div &dv) {
+    if (dv.unit != 0) return (int32_t)(dv.unit > 0 ? num : -num);
+    return (int32_t)((uint32_t)(num >> dv.tz) * (uint32_t)dv.inv);
+}
 
 // Eliminate the pivot columns of `piv_mask` (ascending order) from the lifted
 // matrix in the warp's scratch scr[i*NP + l] (rows 0..K, K = lift row).
@@ -222,6 +227,10 @@ struct WalkArgs {
     uint64_t next_cap;                // capacity of `next`
     unsigned long long *counter;      // work counter
     int64_t limV, limL;               // int64 fast-path bounds (0: always int128)
+    int narrow;                       // D&C walk with int32 storage (tier-0 plans)
+    M128 *ovfl;                       // narrow: cells that left int32 (redone in int64)
+    unsigned long long *ovfl_cnt;
+    uint64_t ovfl_cap;
     unsigned long long *vol;          // D&C walk: [4 limbs of sum |det|, cells] of this level
     unsigned long long *stats;        // [0] ridges tested, [1] ties, [2] inconsistent,
                                       // [3] table full, [4] overflow, [5] boundary ridges,
@@ -235,7 +244,7 @@ struct WalkArgs {
 // re-collected from the table (frontier overflow).
 __device__ __forceinline__ bool insert(M128 *table, uint64_t cap, M128 key, bool &full,
                                        uint8_t *tags = nullptr, uint8_t tag = 0) {
-    uint64_t h = mhash(key) & (cap - 1);
+    uint64_t h = __umul64hi(mhash(key), cap);            // any table size (range reduction)
     const M128 empty = {0, 0};
     const uint64_t max_probe = cap < 4096 ? cap : 4096;   // load <= 3/4: short probes
     for (uint64_t probe = 0; probe < max_probe; ++probe) {
@@ -245,7 +254,7 @@ __device__ __forceinline__ bool insert(M128 *table, uint64_t cap, M128 key, bool
             return true;
         }
         if (old.lo == key.lo && old.hi == key.hi) return false;
-        h = (h + 1) & (cap - 1);
+        h = (h + 1 == cap) ? 0 : h + 1;
     }
     full = true;
     return false;
@@ -371,8 +380,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
 
 // ridge test on a 2-row state (x = remaining V row, y = lift row); inserts the
 // neighbour across the ridge (cell minus p) into the hash set / next frontier
-template <int NPL>
-__device__ __forceinline__ int64_t ridge_step(const int64_t *bx, const int64_t *by, int64_t g, M128 ridge, int p,
+template <int NPL, typename T>
+__device__ __forceinline__ int64_t ridge_step(const T *bx, const T *by, int64_t g, M128 ridge, int p,
                                            int N, int lane, const WalkArgs &a, unsigned long long (&st)[6]) {
     int64_t x[NPL], yk[NPL];
     bool valid[NPL];
@@ -380,8 +389,8 @@ __device__ __forceinline__ int64_t ridge_step(const int64_t *bx, const int64_t *
 #pragma unroll
     for (int q = 0; q < NPL; ++q) {
         const int l = lane + 32 * q;
-        x[q] = bx[l];
-        yk[q] = kappa > 0 ? by[l] : -by[l];
+        x[q] = (int64_t)bx[l];
+        yk[q] = kappa > 0 ? (int64_t)by[l] : -(int64_t)by[l];
         valid[q] = l < N && !mbit(ridge, l);
     }
     ++st[0];
@@ -453,20 +462,46 @@ __device__ __forceinline__ int64_t ridge_step(const int64_t *bx, const int64_t *
 // rows are visited in increasing order.  Column p is written too (it becomes
 // exactly 0): stale values there would feed later steps' inexact divisions
 // and raise false overflow flags.  R <= 32.
-template <int NPL, bool WIDE>
-__device__ __forceinline__ bool dc_eliminate(const int64_t *src, int64_t *dst, int &R, int p, int64_t &prev,
+// T = int32_t (narrow, tier-0 plans): int32 storage, int64 numerators; the
+// range check is on the numerator, |num| < L |prev| <=> |quotient| < L, so
+// no multiply-back is needed (L = limV for V rows, limL for the lift row).
+template <int NPL, bool WIDE, typename T = int64_t>
+__device__ __forceinline__ bool dc_eliminate(const T *src, T *dst, int &R, int p, int64_t &prev,
                                              int lane, bool &ovf, int64_t limV, int64_t limL) {
     constexpr int NP = 32 * NPL;
+    constexpr bool NARROW = sizeof(T) == 4;
     __syncwarp();
-    const int64_t cl = lane < R ? src[lane * NP + p] : 0;
+    const T cl = lane < R ? src[lane * NP + p] : 0;
     const unsigned bal = __ballot_sync(FULL, lane < R - 1 && cl != 0);
     if (bal == 0) return false;
     const int r = __ffs(bal) - 1;
-    const int64_t piv = __shfl_sync(FULL, (long long)cl, r);
     const Div dv = make_div(prev);
-    int64_t prow[NPL];
+    T prow[NPL];
 #pragma unroll
     for (int q = 0; q < NPL; ++q) prow[q] = src[r * NP + lane + 32 * q];
+    if constexpr (NARROW) {
+        const int32_t piv = __shfl_sync(FULL, (int32_t)cl, r);
+        const int64_t ap = prev < 0 ? -prev : prev;
+        const int64_t bV = limV * ap, bL = limL * ap;
+        __syncwarp();
+        for (int i = 0; i < R; ++i) {
+            if (i == r) continue;
+            const int32_t ci = __shfl_sync(FULL, (int32_t)cl, i);
+            const int64_t b = i < R - 1 ? bV : bL;
+            const int o = i == R - 1 ? R - 2 : (i == R - 2 ? r : i);
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int l = lane + 32 * q;
+                const int64_t num = (int64_t)piv * (int64_t)src[i * NP + l] - (int64_t)ci * (int64_t)prow[q];
+                ovf |= (uint64_t)(num + (b - 1)) > (uint64_t)(2 * (b - 1));
+                dst[o * NP + l] = qdiv32u(num, dv);
+            }
+        }
+        --R;
+        prev = piv;
+        return true;
+    }
+    const int64_t piv = __shfl_sync(FULL, (long long)cl, r);
     __syncwarp();   // every lane has read column p before its owner rewrites it
     for (int i = 0; i < R; ++i) {
         if (i == r) continue;
@@ -509,8 +544,8 @@ __host__ __device__ inline int dc_offsets(int K, int *roff) {
 // All K ridges of cell m; false on int64 overflow (the caller retries WIDE).
 // vol = |det| of the cell (the pivot x_p of the first leaf).  Lsm: row-major
 // (K+1) x NP lifted matrix = the depth-0 buffer.
-template <int NPL, bool WIDE>
-__device__ bool dc_cell(const int64_t *Lsm, int64_t *bufs, const int *roff, int K, int N, M128 m, int lane,
+template <int NPL, bool WIDE, typename T = int64_t>
+__device__ bool dc_cell(const T *Lsm, T *bufs, const int *roff, int K, int N, M128 m, int lane,
                         const WalkArgs &a, unsigned long long (&st)[6], int64_t limV, int64_t limL,
                         uint64_t &vol) {
     constexpr int NP = 32 * NPL;
@@ -529,9 +564,9 @@ __device__ bool dc_cell(const int64_t *Lsm, int64_t *bufs, const int *roff, int 
     bool ovf = false;
     vol = 0;
     while (d >= 0) {
-        const int64_t *Bd = d == 0 ? Lsm : bufs + (size_t)roff[d] * NP;
+        const T *Bd = d == 0 ? Lsm : bufs + (size_t)roff[d] * NP;
         if (Bn[d] - A[d] == 1) {
-            const int64_t xp = ridge_step<NPL>(Bd, Bd + NP, prev[d], mclear(m, pts[A[d]]), pts[A[d]], N, lane, a, st);
+            const int64_t xp = ridge_step<NPL, T>(Bd, Bd + NP, prev[d], mclear(m, pts[A[d]]), pts[A[d]], N, lane, a, st);
             if (A[d] == 0) vol = (uint64_t)(xp < 0 ? -xp : xp);
             --d;
             continue;
@@ -540,11 +575,11 @@ __device__ bool dc_cell(const int64_t *Lsm, int64_t *bufs, const int *roff, int 
         const int mid = (A[d] + Bn[d]) / 2;
         const int e0 = stage[d] == 0 ? mid : A[d];       // eliminate [e0, e1)
         const int e1 = stage[d] == 0 ? Bn[d] : mid;
-        int64_t *C = bufs + (size_t)roff[d + 1] * NP;
+        T *C = bufs + (size_t)roff[d + 1] * NP;
         int Rc = R[d];
         int64_t pc = prev[d];
         for (int t = e0; t < e1; ++t) {
-            if (!dc_eliminate<NPL, WIDE>(t == e0 ? Bd : C, C, Rc, pts[t], pc, lane, ovf, limV, limL)) {
+            if (!dc_eliminate<NPL, WIDE, T>(t == e0 ? Bd : C, C, Rc, pts[t], pc, lane, ovf, limV, limL)) {
                 ++st[2];
                 return true;
             }
@@ -563,22 +598,26 @@ __device__ bool dc_cell(const int64_t *Lsm, int64_t *bufs, const int *roff, int 
 
 // One warp per cell of the frontier (walk level); also sums |det| and counts
 // the level's cells (each cell is in exactly one frontier).
-template <int NPL>
+// T = int32_t: narrow storage (tier-0 plans, values |v| < 2^30 / lifts < 2^31);
+// a cell whose values leave int32 goes to a.ovfl and is redone by the int64
+// kernel (neighbours it already inserted were found from checked values).
+template <int NPL, typename T = int64_t>
 __global__ void __launch_bounds__(512) k_walk_dc(WalkArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NP = 32 * NPL;
+    constexpr bool NARROW = sizeof(T) == 4;
     const int K = a.K, N = a.N;
-    int64_t *Lsm = reinterpret_cast<int64_t *>(smem);               // row-major (K+1) x NP
+    T *Lsm = reinterpret_cast<T *>(smem);                           // row-major (K+1) x NP
     for (int t = threadIdx.x; t < (K + 1) * NP; t += blockDim.x) {
         const int i = t / NP, l = t - i * NP;
-        Lsm[t] = l < N ? a.L[(size_t)l * (K + 1) + i] : 0;
+        Lsm[t] = l < N ? (T)a.L[(size_t)l * (K + 1) + i] : 0;
     }
     int roff[kDcDepth + 1];
     const int rows_total = dc_offsets(K, roff);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // roff[d] for d >= 1 counts from roff[1] = 0
-    int64_t *bufs = Lsm + (size_t)(K + 1) * NP + (size_t)warp * rows_total * NP;
+    T *bufs = Lsm + (size_t)(K + 1) * NP + (size_t)warp * rows_total * NP;
     unsigned long long st[6] = {0, 0, 0, 0, 0, 0};
     uint64_t lo = 0, hi = 0, cells = 0, fallbacks = 0;
     for (;;) {
@@ -588,12 +627,22 @@ __global__ void __launch_bounds__(512) k_walk_dc(WalkArgs a) {
         if (idx >= a.ncur) break;
         const M128 m = a.cur[idx];
         uint64_t v = 0;
-        bool done = false;
-        if (a.limV > 0) done = dc_cell<NPL, false>(Lsm, bufs, roff, K, N, m, lane, a, st, a.limV, a.limL, v);
-        fallbacks += !done;
-        if (!done && !dc_cell<NPL, true>(Lsm, bufs, roff, K, N, m, lane, a, st, 0, 0, v)) {
-            ++st[4];
-            continue;
+        if constexpr (NARROW) {
+            if (!dc_cell<NPL, false, T>(Lsm, bufs, roff, K, N, m, lane, a, st, a.limV, a.limL, v)) {
+                if (lane == 0) {
+                    const unsigned long long pos = atomicAdd(a.ovfl_cnt, 1ull);
+                    if (pos < a.ovfl_cap) a.ovfl[pos] = m;
+                }
+                continue;
+            }
+        } else {
+            bool done = false;
+            if (a.limV > 0) done = dc_cell<NPL, false>(Lsm, bufs, roff, K, N, m, lane, a, st, a.limV, a.limL, v);
+            fallbacks += !done;
+            if (!done && !dc_cell<NPL, true>(Lsm, bufs, roff, K, N, m, lane, a, st, 0, 0, v)) {
+                ++st[4];
+                continue;
+            }
         }
         const uint64_t t = lo + v;
         hi += t < lo;
@@ -681,6 +730,16 @@ __global__ void k_rehash(const M128 *old, const uint8_t *old_tags, uint64_t oldc
     }
 }
 
+// insert a list of cells (one level of the walk, tagged) into the table
+__global__ void k_insert_list(const M128 *list, uint64_t n, M128 *tab, uint8_t *tags, uint64_t cap, uint8_t tag,
+                              unsigned long long *full_flag) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        bool full = false;
+        insert(tab, cap, list[i], full, tags, tag);
+        if (full) atomicAdd(full_flag, 1ull);
+    }
+}
+
 // the cells of one level (by tag) into out[0, *cnt)
 __global__ void k_collect(const M128 *tab, const uint8_t *tags, uint64_t cap, uint8_t tag, M128 *out,
                           unsigned long long *cnt) {
@@ -710,6 +769,15 @@ int launch_rehash(const void *old, const uint8_t *old_tags, uint64_t oldcap, voi
     return (int)cudaGetLastError();
 }
 
+int launch_insert_list(const void *list, uint64_t n, void *tab, uint8_t *tags, uint64_t cap, uint8_t tag,
+                       unsigned long long *full_flag, void *stream) {
+    if (n == 0) return 0;
+    walk::k_insert_list<<<1184, 256, 0, (cudaStream_t)stream>>>((const walk::M128 *)list, n, (walk::M128 *)tab,
+                                                                tags, cap, tag, full_flag);
+    launch_counter_add(1);
+    return (int)cudaGetLastError();
+}
+
 int launch_collect(const void *tab, const uint8_t *tags, uint64_t cap, uint8_t tag, void *out,
                    unsigned long long *cnt, void *stream) {
     walk::k_collect<<<1184, 256, 0, (cudaStream_t)stream>>>((const walk::M128 *)tab, tags, cap, tag,
@@ -728,6 +796,25 @@ size_t walk_smem_bytes(int K, int N) {
 // memory); *fused = 1 then (the launch also summed the level's volumes).
 template <int NPL>
 static int walk_npl(const walk::WalkArgs &a, int grid, size_t smem, int *fused) {
+    if (a.narrow && a.K <= 31 && !std::getenv("BDEG_WALK_SCRATCH")) {
+        const size_t lb = (size_t)(a.K + 1) * 32 * NPL * 4;
+        const size_t pw = (size_t)walk::dc_offsets(a.K, nullptr) * 32 * NPL * 4;
+        const size_t budget = 227 * 1024;
+        const int nw = lb + pw > budget ? 0 : (int)std::min<size_t>(16, (budget - lb) / pw);
+        if (nw >= 2) {
+            const size_t dsmem = lb + (size_t)nw * pw;
+            cudaError_t e = cudaFuncSetAttribute((const void *)walk::k_walk_dc<NPL, int32_t>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+            if (e != cudaSuccess) return (int)e;
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int per_sm = std::max<int>(1, (int)((228 * 1024) / (dsmem + 1024)));
+            walk::k_walk_dc<NPL, int32_t><<<sms * per_sm, nw * 32, dsmem, (cudaStream_t)a.stream>>>(a);
+            *fused = 2;
+            return (int)cudaGetLastError();
+        }
+    }
     const size_t lbytes = (size_t)(a.K + 1) * 32 * NPL * 8;
     const size_t per_warp = (size_t)walk::dc_offsets(a.K, nullptr) * 32 * NPL * 8;
     const size_t budget = 227 * 1024;
@@ -757,8 +844,13 @@ static int walk_npl(const walk::WalkArgs &a, int grid, size_t smem, int *fused) 
 int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, void *next,
                 unsigned long long *next_cnt, void *table, uint64_t cap, unsigned long long *counter,
                 unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL,
-                unsigned long long *vol, int *fused, uint8_t *tags, unsigned tag, uint64_t next_cap) {
+                unsigned long long *vol, int *fused, uint8_t *tags, unsigned tag, uint64_t next_cap,
+                int narrow, void *ovfl, unsigned long long *ovfl_cnt, uint64_t ovfl_cap) {
     walk::WalkArgs a;
+    a.narrow = narrow;
+    a.ovfl = (walk::M128 *)ovfl;
+    a.ovfl_cnt = ovfl_cnt;
+    a.ovfl_cap = ovfl_cap;
     a.vol = vol;
     a.tags = tags;
     a.tag = (uint8_t)tag;
