@@ -11,3 +11,6 @@ for lib in scratch/libbdeg_mb5.so; do
   done
 done
 ls $OUT
+export BDEG_DEBUG=1 BDEG_DEBUG_LEVELS=1
+WALK_SEED=2 timeout 1800 python tools/walk_runs.py w55 > $OUT/walk_w55_seed2.log 2>&1; echo "w55 s2 rc $?"; tail -1 $OUT/walk_w55_seed2.log | cut -c1-300
+WALK_SEED=2 timeout 1200 python tools/walk_runs.py w38 > $OUT/walk_w38_seed2.log 2>&1; echo "w38 s2 rc $?"; tail -1 $OUT/walk_w38_seed2.log | cut -c1-300
