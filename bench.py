@@ -285,6 +285,12 @@ def run_gpu(args):
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             traffic = json.load(open(tp)).get(args.workload)
+        # executed-instruction utilisation of the same kernel from the committed
+        # ncu --set full capture (the counter-backed side of the roofline)
+        executed = None
+        ep = os.path.join(ROOT, "profiles", "ncu_executed.json")
+        if os.path.exists(ep):
+            executed = json.load(open(ep)).get(args.workload)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             v, cores, sample = cpu_oracle_sample(K, V, w, args.ref_sample)
@@ -308,7 +314,7 @@ def run_gpu(args):
                          "unit": "Tintop/s", "frac": achieved / peak_ops, "traffic": traffic,
                          "peak_basis": f"128 int lane-ops/clk/SM x {n_sm} SMs x {sm_mhz:.0f} MHz "
                                        f"({peak_kind} sm_max_mhz) x {world} GPU(s)",
-                         "algorithmic_ops_per_step": alg_ops},
+                         "algorithmic_ops_per_step": alg_ops, "ncu_executed": executed},
             "cpu_baseline": cpu,
             "e2e": {"value": total / (e2e_step / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
