@@ -382,7 +382,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
 // neighbour across the ridge (cell minus p) into the hash set / next frontier
 template <int NPL, typename T>
 __device__ __forceinline__ int64_t ridge_step(const T *bx, const T *by, int64_t g, M128 ridge, int p,
-                                           int N, int lane, const WalkArgs &a, unsigned long long (&st)[6]) {
+                                           int N, int lane, const WalkArgs &a, unsigned long long (&st)[6],
+                                           int &nb) {
+    nb = -1;
     int64_t x[NPL], yk[NPL];
     bool valid[NPL];
     const int kappa = g > 0 ? 1 : -1;
@@ -443,16 +445,32 @@ __device__ __forceinline__ int64_t ridge_step(const T *bx, const T *by, int64_t 
     }
     if (tie) ++st[1];
     if (found < 0) { if (!tie) ++st[5]; return xp; }
-    if (lane == 0) {
-        const M128 nm = mset(ridge, found);
-        bool full = false;
-        if (insert(a.table, a.cap, nm, full, a.tags, a.tag)) {
-            const unsigned long long pos = atomicAdd(a.next_cnt, 1ull);
+    nb = found;                                   // inserted by dc_cell, batched per cell
+    return xp;
+}
+
+// Insert the neighbours found by a cell's ridge tests, one per lane (lane t
+// holds ridge t's neighbour point, or -1): up to K concurrent 128-bit CAS
+// probes instead of K serial ones, and one warp-aggregated frontier append.
+__device__ __forceinline__ void insert_neighbours(M128 m, int my_p, int my_nb, int lane, const WalkArgs &a,
+                                                  unsigned long long (&st)[6]) {
+    bool isnew = false, full = false;
+    M128 nm = {0, 0};
+    if (my_nb >= 0) {
+        nm = mset(mclear(m, my_p), my_nb);
+        isnew = insert(a.table, a.cap, nm, full, a.tags, a.tag);
+    }
+    const unsigned nmask = __ballot_sync(FULL, isnew);
+    if (nmask) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.next_cnt, (unsigned long long)__popc(nmask));
+        base = __shfl_sync(FULL, base, 0);
+        if (isnew) {
+            const unsigned long long pos = base + __popc(nmask & ((1u << lane) - 1));
             if (pos < a.next_cap) a.next[pos] = nm;   // else re-collected by tag
         }
-        if (full) ++st[3];
     }
-    return xp;
+    st[3] += __popc(__ballot_sync(FULL, full));
 }
 
 // Eliminate pivot column p: rows of src (R rows, V rows [0, R-1), lift row
@@ -483,20 +501,28 @@ __device__ __forceinline__ bool dc_eliminate(const T *src, T *dst, int &R, int p
         const int32_t piv = __shfl_sync(FULL, (int32_t)cl, r);
         const int64_t ap = prev < 0 ? -prev : prev;
         const int64_t bV = limV * ap, bL = limL * ap;
+        // branch-free exact quotient: for d = +-1, tz = 0 and inv = d^-1 = d
+        const int tz = dv.unit != 0 ? 0 : dv.tz;
+        const uint32_t inv = dv.unit > 0 ? 1u : (dv.unit < 0 ? 0xFFFFFFFFu : (uint32_t)dv.inv);
         __syncwarp();
-        for (int i = 0; i < R; ++i) {
-            if (i == r) continue;
+        // rows in increasing order (in place: see above); V rows keep their slot
+        // except the last one, which takes the pivot row's; the lift row moves
+        // to R-2 — no per-row selects in the loops
+        auto row = [&](int i, int o, int64_t b) {
             const int32_t ci = __shfl_sync(FULL, (int32_t)cl, i);
-            const int64_t b = i < R - 1 ? bV : bL;
-            const int o = i == R - 1 ? R - 2 : (i == R - 2 ? r : i);
+            const int64_t b1 = b - 1, b2 = 2 * (b - 1);
 #pragma unroll
             for (int q = 0; q < NPL; ++q) {
                 const int l = lane + 32 * q;
                 const int64_t num = (int64_t)piv * (int64_t)src[i * NP + l] - (int64_t)ci * (int64_t)prow[q];
-                ovf |= (uint64_t)(num + (b - 1)) > (uint64_t)(2 * (b - 1));
-                dst[o * NP + l] = qdiv32u(num, dv);
+                ovf |= (uint64_t)(num + b1) > (uint64_t)b2;
+                dst[o * NP + l] = (int32_t)((uint32_t)(num >> tz) * inv);
             }
-        }
+        };
+        for (int i = 0; i < r; ++i) row(i, i, bV);
+        for (int i = r + 1; i < R - 2; ++i) row(i, i, bV);
+        if (r != R - 2) row(R - 2, r, bV);
+        row(R - 1, R - 2, bL);
         --R;
         prev = piv;
         return true;
@@ -563,10 +589,14 @@ __device__ bool dc_cell(const T *Lsm, T *bufs, const int *roff, int K, int N, M1
     A[0] = 0; Bn[0] = K; stage[0] = 0; R[0] = K + 1; prev[0] = 1;
     bool ovf = false;
     vol = 0;
+    int my_p = -1, my_nb = -1;        // lane t: ridge t's dropped point and neighbour
     while (d >= 0) {
         const T *Bd = d == 0 ? Lsm : bufs + (size_t)roff[d] * NP;
         if (Bn[d] - A[d] == 1) {
-            const int64_t xp = ridge_step<NPL, T>(Bd, Bd + NP, prev[d], mclear(m, pts[A[d]]), pts[A[d]], N, lane, a, st);
+            int nb;
+            const int64_t xp = ridge_step<NPL, T>(Bd, Bd + NP, prev[d], mclear(m, pts[A[d]]), pts[A[d]], N, lane,
+                                                  a, st, nb);
+            if (lane == A[d]) { my_p = pts[A[d]]; my_nb = nb; }
             if (A[d] == 0) vol = (uint64_t)(xp < 0 ? -xp : xp);
             --d;
             continue;
@@ -581,9 +611,10 @@ __device__ bool dc_cell(const T *Lsm, T *bufs, const int *roff, int K, int N, M1
         for (int t = e0; t < e1; ++t) {
             if (!dc_eliminate<NPL, WIDE, T>(t == e0 ? Bd : C, C, Rc, pts[t], pc, lane, ovf, limV, limL)) {
                 ++st[2];
+                insert_neighbours(m, my_p, my_nb, lane, a, st);
                 return true;
             }
-            if (__any_sync(FULL, ovf)) return false;
+            if (__any_sync(FULL, ovf)) return false;   // nothing inserted: the caller redoes the cell
         }
         A[d + 1] = stage[d] == 0 ? A[d] : mid;
         Bn[d + 1] = stage[d] == 0 ? mid : Bn[d];
@@ -593,6 +624,7 @@ __device__ bool dc_cell(const T *Lsm, T *bufs, const int *roff, int K, int N, M1
         R[d] = Rc;
         prev[d] = pc;
     }
+    insert_neighbours(m, my_p, my_nb, lane, a, st);
     return true;
 }
 
