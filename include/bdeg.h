@@ -189,7 +189,15 @@ bdeg_status bdeg_cell_normal(bdeg_plan_t plan, uint64_t mask_lo, uint64_t mask_h
  * instead of C(N,K).  Result: degree and cells exact (same subdivision as
  * bdeg_degree for the same lifting); candidates/singular are not enumerated
  * (singular_complete = 0); leaves = ridge tests, dead_leaves = boundary ridges.
- * Re-lifts generated liftings on ties like bdeg_degree. */
+ * Re-lifts generated liftings on ties like bdeg_degree.
+ * Memory: device buffers allocated by the call itself (cudaMalloc, freed on
+ * return) — a hash set of 16-byte cell masks + 1-byte level tags that holds
+ * only the breadth-first window of levels L-1..L+1 (adjacent cells' levels
+ * differ by <= 1), plus two frontier buffers; it grows to the free device
+ * memory and fails with BDEG_E_TOO_LARGE when two consecutive levels no
+ * longer fit.  N <= 128 points (N > 64 needs a generated lifting: the start
+ * cell is a basis lifted at 0).  Tier-0 plans use int32 working storage
+ * (cells whose values leave int32 are redone in int64, exact either way). */
 bdeg_status bdeg_degree_walk(bdeg_plan_t plan, bdeg_result *out);
 
 /* Cross-GPU dynamic work stealing.  One process (rank 0)
