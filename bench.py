@@ -138,7 +138,9 @@ def run_reference(args):
         return
     desc, K, V, w, extra = workload(args.workload)
     total = math.comb(len(V), K)
-    budget = args.ref_sample
+    # each step is a bounded sample; the whole --steps/--warmup run stays at
+    # ~2.4e8 candidates (about 3 minutes of the oracle on 16 host cores)
+    budget = int(min(args.ref_sample, max(2e5, 2.4e8 / (args.steps + args.warmup / 4.0))))
     for _ in range(args.warmup):
         cpu_oracle_sample(K, V, w, budget // 4, seed=1)
     vals = []

@@ -529,11 +529,9 @@ __device__ __forceinline__ bool dc_eliminate(const T *src, T *dst, int &R, int p
     }
     const int64_t piv = __shfl_sync(FULL, (long long)cl, r);
     __syncwarp();   // every lane has read column p before its owner rewrites it
-    for (int i = 0; i < R; ++i) {
-        if (i == r) continue;
+    // same row order and slot mapping as the narrow path, without per-row selects
+    auto row = [&](int i, int o, int64_t lim) {
         const int64_t ci = __shfl_sync(FULL, (long long)cl, i);
-        const int64_t lim = i < R - 1 ? limV : limL;
-        const int o = i == R - 1 ? R - 2 : (i == R - 2 ? r : i);
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
             const int l = lane + 32 * q;
@@ -546,7 +544,11 @@ __device__ __forceinline__ bool dc_eliminate(const T *src, T *dst, int &R, int p
             }
             dst[o * NP + l] = v;
         }
-    }
+    };
+    for (int i = 0; i < r; ++i) row(i, i, limV);
+    for (int i = r + 1; i < R - 2; ++i) row(i, i, limV);
+    if (r != R - 2) row(R - 2, r, limV);
+    row(R - 1, R - 2, limL);
     --R;
     prev = piv;
     return true;
