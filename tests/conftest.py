@@ -35,8 +35,13 @@ def _ensure_built():
     fresh checkout lacks it (nvcc cross-compiles for sm_100a without a GPU)."""
     lib = os.path.join(ROOT, "paper_1501_02237_b200", "libbdeg.so")
     if not os.path.exists(lib):
-        from paper_1501_02237_b200._build import build_lib
-        build_lib()
+        # load _build.py by path: importing the package would need the library
+        import importlib.util
+        spec = importlib.util.spec_from_file_location(
+            "_bdeg_build", os.path.join(ROOT, "paper_1501_02237_b200", "_build.py"))
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        mod.build_lib()
 
 
 _ensure_built()
