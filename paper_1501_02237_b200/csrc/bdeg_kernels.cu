@@ -67,7 +67,7 @@ __device__ __forceinline__ Div make_div(int64_t d) {
     r.d = d;
     r.unit = (d == 1) ? 1 : (d == -1 ? -1 : 0);
     r.tz = 0;
-    r.inv = 1;
+    r.inv = d < 0 ? ~0ull : 1ull;   // d = +-1: (num >> 0) * inv is the quotient, branch-free
     if (r.unit == 0) {
         r.tz = __ffsll(d) - 1;
         const uint64_t o = (uint64_t)(d >> r.tz);
@@ -111,8 +111,11 @@ __device__ __forceinline__ bool within(int64_t num, int64_t b) {
 // Exact quotient whose range was established from the numerator (|num| <
 // L * |d| implies |q| < L): no multiply-back is needed.
 __device__ __forceinline__ int32_t qdiv32u(int64_t num, const Div &dv) {
-    if (dv.unit != 0) return (int32_t)(dv.unit > 0 ? num : -num);
-    return (int32_t)((uint32_t)(num >> dv.tz) * (uint32_t)dv.inv);
+    return (int32_t)((uint32_t)(num >> dv.tz) * (uint32_t)dv.inv);   // also d = +-1 (tz 0, inv +-1)
+}
+// same for an int64 quotient (tier-1 lift row), branch-free
+__device__ __forceinline__ int64_t qdiv64u(int64_t num, const Div &dv) {
+    return (int64_t)((uint64_t)(num >> dv.tz) * dv.inv);
 }
 __device__ __forceinline__ int64_t qdiv128(i128 num, const Div &dv, bool &ovf) {
     int64_t q;
@@ -356,7 +359,7 @@ __device__ __forceinline__ void elim_step(const typename Tr<TIER>::VV (&sv)[NPL]
         } else {
             const int64_t num = (int64_t)piv * (int64_t)sl[q] - (int64_t)cl * (int64_t)prow;
             ovf |= !within(num, bL);
-            ol[q] = (VL)qdiv64(num, dv);
+            ol[q] = (VL)qdiv64u(num, dv);
         }
     }
 }
@@ -726,7 +729,7 @@ __device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, co
                     } else {
                         const int64_t num = piv * scr[i * NP + l] - ci * scr[r * NP + l];
                         o |= !within(num, b);
-                        scr[i * NP + l] = qdiv64(num, dv);
+                        scr[i * NP + l] = qdiv64u(num, dv);
                     }
                 }
             }
