@@ -34,6 +34,7 @@ struct bdeg_plan_s {
     int tier = 0, S = 0, T = 0, D = 0;
     int bits_v = 30, bits_l = 31;
     bool big = false;                 // N > 64: walk only (rank space beyond uint64 / lane slots)
+    bool v_safe = false;              // every V-minor < 2^31 - 1 by Hadamard's bound (tier-0 kernels skip V checks)
     unsigned long long *steal = nullptr;   // cross-GPU item counters (2, by step parity), IPC-mapped
     int steal_parity = 0;
     uint64_t basis_lo = 0, basis_hi = 0;   // basis-seeded start cell (N > 64, generated lifting)
@@ -194,6 +195,27 @@ void choose_tier_and_blocks(bdeg_plan_s *p) {
     if (bv <= 28 && bl <= 28) p->tier = 0;
     else if (bv + 2 <= 30 && bl < p->bits_l) p->tier = 1;
     else p->tier = 2;
+    // Hadamard: |det| <= prod of the column norms, so every V-minor (any rows,
+    // <= K columns; every V-row value of the elimination is one, by Sylvester's
+    // identity) is at most sqrt(product of the K largest squared column norms)
+    {
+        std::vector<u128> n2(p->N, 0);
+        const u128 cap = (u128)1 << 124;
+        for (int l = 0; l < p->N; ++l)
+            for (int i = 0; i < p->K; ++i) {
+                const int64_t v = p->V[(size_t)l * p->K + i];
+                const u128 a = (u128)(v < 0 ? -(i128)v : (i128)v);
+                n2[l] = std::min(cap, n2[l] + (a > ((u128)1 << 62) ? cap : a * a));
+            }
+        std::sort(n2.begin(), n2.end(), [](u128 x, u128 y) { return x > y; });
+        u128 prod = 1;
+        for (int i = 0; i < std::min(p->K, p->N) && prod < cap; ++i) {
+            const u128 f = n2[i] == 0 ? 1 : n2[i];
+            prod = (f > cap / prod) ? cap : prod * f;
+        }
+        const u128 lim = (u128)INT32_MAX * (u128)INT32_MAX;
+        p->v_safe = prod < lim && !std::getenv("BDEG_NO_VSAFE");
+    }
     if (p->opt.flags & BDEG_FLAG_FORCE_TIER0) p->tier = 0;
     if (p->opt.flags & BDEG_FLAG_FORCE_TIER1) p->tier = 1;
     if (p->opt.flags & BDEG_FLAG_FORCE_TIER2) p->tier = 2;
@@ -441,6 +463,7 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     a.grid = p->grid;
     a.stream = st;
     a.tier = force_tier >= 0 ? force_tier : p->tier;
+    if (a.tier == 0 && p->v_safe) a.tier = 3;   // tier 0 without V-row range checks (Hadamard)
     a.bits_v = p->bits_v;
     a.degree_only = (p->opt.flags & BDEG_FLAG_DEGREE_ONLY) ? 1 : 0;
     a.cells_out = cells_out;

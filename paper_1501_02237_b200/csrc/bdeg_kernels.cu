@@ -49,6 +49,10 @@ constexpr int kWarps = 4;           // warps per CTA
 // its tier is re-run in tier 2 (replay launch).
 template <int TIER> struct Tr;
 template <> struct Tr<0> { typedef int32_t VV; typedef int32_t VL; };
+// tier 3 = tier 0 for a plan whose V-minors are all < 2^31 by Hadamard's
+// bound (host-proved): V-row range checks are omitted, the lift
+// row is still checked
+template <> struct Tr<3> { typedef int32_t VV; typedef int32_t VL; };
 template <> struct Tr<1> { typedef int32_t VV; typedef int64_t VL; };
 template <> struct Tr<2> { typedef int64_t VV; typedef int64_t VL; };
 
@@ -346,13 +350,13 @@ __device__ __forceinline__ void elim_step(const typename Tr<TIER>::VV (&sv)[NPL]
             } else {
                 // |num| < bV = L |prev|  <=>  |quotient| < L (tier bound)
                 const int64_t num = madw(piv, s, mulw(-cs, prow));
-                ovf |= !within(num, bV);
+                if constexpr (TIER != 3) ovf |= !within(num, bV);
                 ov[q][o] = qdiv32u(num, dv);
             }
         }
         if constexpr (TIER == 2) {
             ol[q] = qdiv128((i128)piv * sl[q] - (i128)cl * prow, dv, ovf);
-        } else if constexpr (TIER == 0) {
+        } else if constexpr (TIER == 0 || TIER == 3) {
             const int64_t num = madw(piv, sl[q], mulw(-cl, prow));
             ovf |= !within(num, bL);
             ol[q] = qdiv32u(num, dv);
@@ -484,7 +488,7 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
             const VV prow = p0 ? sv[q][0] : sv[q][1];
             const VV s = p0 ? sv[q][1] : sv[q][0];
             X[q] = madw(piv, s, mulw(ncs, prow));
-            if constexpr (TIER == 0) Y[q] = madw(pz, sl[q], mulw(ncz, prow));
+            if constexpr (TIER == 0 || TIER == 3) Y[q] = madw(pz, sl[q], mulw(ncz, prow));
             else Y[q] = (int64_t)pz * (int64_t)sl[q] + (int64_t)ncz * (int64_t)prow;
             fx[q] = opaque((float)X[q]);
             const float fy = opaque((float)Y[q]);
@@ -571,8 +575,8 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
     if constexpr (RV > 2 || TIER == 2) dv = make_div(prev);
     if constexpr (TIER != 2) {
         const int64_t ap = prev < 0 ? -prev : prev;
-        bV = (TIER == 0 ? (int64_t)INT32_MAX : cx.limV) * ap;
-        bL = (TIER == 0 ? (int64_t)INT32_MAX : cx.limL) * ap;
+        bV = ((TIER == 0 || TIER == 3) ? (int64_t)INT32_MAX : cx.limV) * ap;
+        bL = ((TIER == 0 || TIER == 3) ? (int64_t)INT32_MAX : cx.limL) * ap;
     }
     for (int c = lo; c < hi; ++c) {
         const uint64_t nb = base + cx.C(c, i + 1);
@@ -713,8 +717,8 @@ __device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, co
             // checked), so numerators are exact in int64 and |num| < L |prev|
             // <=> |quotient| < L; tier 2: int128 numerators, quotients verified
             const int64_t ap = prev < 0 ? -prev : prev;
-            const int64_t bV = (TIER == 0 ? (int64_t)INT32_MAX : cx.limV) * ap;
-            const int64_t bL = (TIER == 0 ? (int64_t)INT32_MAX : cx.limL) * ap;
+            const int64_t bV = ((TIER == 0 || TIER == 3) ? (int64_t)INT32_MAX : cx.limV) * ap;
+            const int64_t bL = ((TIER == 0 || TIER == 3) ? (int64_t)INT32_MAX : cx.limL) * ap;
             for (int i = 0; i <= K; ++i) {
                 if (i == r || (i < K && !((alive >> i) & 1ull))) continue;
                 const int64_t ci = scr[i * NP + p];
@@ -728,7 +732,7 @@ __device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, co
                         scr[i * NP + l] = qdiv128(num, dv, o);
                     } else {
                         const int64_t num = piv * scr[i * NP + l] - ci * scr[r * NP + l];
-                        o |= !within(num, b);
+                        if (TIER != 3 || i == K) o |= !within(num, b);
                         scr[i * NP + l] = qdiv64u(num, dv);
                     }
                 }
@@ -754,7 +758,7 @@ __device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, co
 #pragma unroll
                     for (int q = 0; q < NPL; ++q) {
                         const int64_t v = scr[i * NP + lane + 32 * q];
-                        if constexpr (TIER == 0) o |= !inside(v, (int64_t)1 << 31);
+                        if constexpr (TIER == 0 || TIER == 3) o |= !inside(v, (int64_t)1 << 31);
                         if constexpr (TIER == 1) o |= !inside(v, cx.limV);
                         sv[q][kk] = (VV)v;
                     }
@@ -763,7 +767,7 @@ __device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, co
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
             const int64_t v = scr[K * NP + lane + 32 * q];
-            if constexpr (TIER == 0) o |= !inside(v, (int64_t)1 << 31);
+            if constexpr (TIER == 0 || TIER == 3) o |= !inside(v, (int64_t)1 << 31);
             if constexpr (TIER == 1) o |= !inside(v, cx.limL);
             sl[q] = (VL)v;
         }
@@ -774,12 +778,12 @@ __device__ void process_item(uint64_t item, const int64_t *Lsm, int64_t *scr, co
 #pragma unroll
             for (int kk = 0; kk < S + 1; ++kk) {
                 const int64_t v = (l < N) ? Lsm[l * (K + 1) + kk] : 0;
-                if constexpr (TIER == 0) o |= !inside(v, (int64_t)1 << 31);
+                if constexpr (TIER == 0 || TIER == 3) o |= !inside(v, (int64_t)1 << 31);
                 if constexpr (TIER == 1) o |= !inside(v, cx.limV);
                 sv[q][kk] = (VV)v;
             }
             const int64_t v = (l < N) ? Lsm[l * (K + 1) + K] : 0;
-            if constexpr (TIER == 0) o |= !inside(v, (int64_t)1 << 31);
+            if constexpr (TIER == 0 || TIER == 3) o |= !inside(v, (int64_t)1 << 31);
             if constexpr (TIER == 1) o |= !inside(v, cx.limL);
             sl[q] = (VL)v;
         }
@@ -962,6 +966,7 @@ static KernFn pick(int tier, int npl, int S) {
 #define BDEG_KS(T_, P_) BDEG_K(T_, P_, 0) BDEG_K(T_, P_, 1) BDEG_K(T_, P_, 2) BDEG_K(T_, P_, 3) \
     BDEG_K(T_, P_, 4) BDEG_K(T_, P_, 5) BDEG_K(T_, P_, 6)
     BDEG_KS(0, 1) BDEG_KS(0, 2) BDEG_KS(1, 1) BDEG_KS(1, 2) BDEG_KS(2, 1) BDEG_KS(2, 2)
+    BDEG_KS(3, 1) BDEG_KS(3, 2)
 #undef BDEG_KS
 #undef BDEG_K
     return nullptr;
