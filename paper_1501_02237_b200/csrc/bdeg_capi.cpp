@@ -764,7 +764,7 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
             }
             int rc = launch_walk(p->d_L, K, p->N, cur.p, ncur, nxt.p, next_cnt, table.p, cap, counter, stats,
                                  grid, st, limV, limL, lvol, &fused, (uint8_t *)tags.p, tag, ncap,
-                                 narrow, ovfl.p, aux.u() + 15, ovfl_cap);
+                                 narrow, ovfl.p, aux.u() + 15, ovfl_cap, p->v_safe ? 1 : 0);
             if (rc) return fail(p, BDEG_E_CUDA, std::string("k_walk: ") + cudaGetErrorString((cudaError_t)rc));
             cudaMemcpyAsync(h, aux.p, 16 * 8, cudaMemcpyDeviceToHost, st);
             cudaError_t ce = cudaStreamSynchronize(st);

@@ -115,7 +115,7 @@ int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, 
                 unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL,
                 unsigned long long *vol, int *fused, uint8_t *tags, unsigned tag, uint64_t next_cap,
                 int narrow = 0, void *ovfl = nullptr, unsigned long long *ovfl_cnt = nullptr,
-                uint64_t ovfl_cap = 0);
+                uint64_t ovfl_cap = 0, int vsafe = 0);
 int launch_cellvol(const int64_t *L, int K, int N, const void *table, uint64_t cap, unsigned long long *out,
                    unsigned long long *counter, int grid, void *stream, int64_t limV, int64_t limL);
 int launch_rehash(const void *old, const uint8_t *old_tags, uint64_t oldcap, void *tab, uint8_t *tags, uint64_t cap,

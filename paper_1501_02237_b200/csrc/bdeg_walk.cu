@@ -228,6 +228,7 @@ struct WalkArgs {
     unsigned long long *counter;      // work counter
     int64_t limV, limL;               // int64 fast-path bounds (0: always int128)
     int narrow;                       // D&C walk with int32 storage (tier-0 plans)
+    int vsafe;                        // V-minors < 2^31 by Hadamard (host): no V-row range checks
     M128 *ovfl;                       // narrow: cells that left int32 (redone in int64)
     unsigned long long *ovfl_cnt;
     uint64_t ovfl_cap;
@@ -483,7 +484,7 @@ __device__ __forceinline__ void insert_neighbours(M128 m, int my_p, int my_nb, i
 // T = int32_t (narrow, tier-0 plans): int32 storage, int64 numerators; the
 // range check is on the numerator, |num| < L |prev| <=> |quotient| < L, so
 // no multiply-back is needed (L = limV for V rows, limL for the lift row).
-template <int NPL, bool WIDE, typename T = int64_t>
+template <int NPL, bool WIDE, typename T = int64_t, bool VSAFE = false>
 __device__ __forceinline__ bool dc_eliminate(const T *src, T *dst, int &R, int p, int64_t &prev,
                                              int lane, bool &ovf, int64_t limV, int64_t limL) {
     constexpr int NP = 32 * NPL;
@@ -508,21 +509,23 @@ __device__ __forceinline__ bool dc_eliminate(const T *src, T *dst, int &R, int p
         // rows in increasing order (in place: see above); V rows keep their slot
         // except the last one, which takes the pivot row's; the lift row moves
         // to R-2 — no per-row selects in the loops
-        auto row = [&](int i, int o, int64_t b) {
+        auto row = [&](int i, int o, int64_t b, bool chk) {
             const int32_t ci = __shfl_sync(FULL, (int32_t)cl, i);
             const int64_t b1 = b - 1, b2 = 2 * (b - 1);
 #pragma unroll
             for (int q = 0; q < NPL; ++q) {
                 const int l = lane + 32 * q;
                 const int64_t num = (int64_t)piv * (int64_t)src[i * NP + l] - (int64_t)ci * (int64_t)prow[q];
-                ovf |= (uint64_t)(num + b1) > (uint64_t)b2;
+                if (chk) ovf |= (uint64_t)(num + b1) > (uint64_t)b2;
                 dst[o * NP + l] = (int32_t)((uint32_t)(num >> tz) * inv);
             }
         };
-        for (int i = 0; i < r; ++i) row(i, i, bV);
-        for (int i = r + 1; i < R - 2; ++i) row(i, i, bV);
-        if (r != R - 2) row(R - 2, r, bV);
-        row(R - 1, R - 2, bL);
+        // V rows need no check when Hadamard bounds every V-minor below 2^31
+        const bool cv = !VSAFE;
+        for (int i = 0; i < r; ++i) row(i, i, bV, cv);
+        for (int i = r + 1; i < R - 2; ++i) row(i, i, bV, cv);
+        if (r != R - 2) row(R - 2, r, bV, cv);
+        row(R - 1, R - 2, bL, true);
         --R;
         prev = piv;
         return true;
@@ -572,7 +575,7 @@ __host__ __device__ inline int dc_offsets(int K, int *roff) {
 // All K ridges of cell m; false on int64 overflow (the caller retries WIDE).
 // vol = |det| of the cell (the pivot x_p of the first leaf).  Lsm: row-major
 // (K+1) x NP lifted matrix = the depth-0 buffer.
-template <int NPL, bool WIDE, typename T = int64_t>
+template <int NPL, bool WIDE, typename T = int64_t, bool VSAFE = false>
 __device__ bool dc_cell(const T *Lsm, T *bufs, const int *roff, int K, int N, M128 m, int lane,
                         const WalkArgs &a, unsigned long long (&st)[6], int64_t limV, int64_t limL,
                         uint64_t &vol) {
@@ -611,7 +614,7 @@ __device__ bool dc_cell(const T *Lsm, T *bufs, const int *roff, int K, int N, M1
         int Rc = R[d];
         int64_t pc = prev[d];
         for (int t = e0; t < e1; ++t) {
-            if (!dc_eliminate<NPL, WIDE, T>(t == e0 ? Bd : C, C, Rc, pts[t], pc, lane, ovf, limV, limL)) {
+            if (!dc_eliminate<NPL, WIDE, T, VSAFE>(t == e0 ? Bd : C, C, Rc, pts[t], pc, lane, ovf, limV, limL)) {
                 ++st[2];
                 insert_neighbours(m, my_p, my_nb, lane, a, st);
                 return true;
@@ -635,7 +638,7 @@ __device__ bool dc_cell(const T *Lsm, T *bufs, const int *roff, int K, int N, M1
 // T = int32_t: narrow storage (tier-0 plans, values |v| < 2^30 / lifts < 2^31);
 // a cell whose values leave int32 goes to a.ovfl and is redone by the int64
 // kernel (neighbours it already inserted were found from checked values).
-template <int NPL, typename T = int64_t>
+template <int NPL, typename T = int64_t, bool VSAFE = false>
 __global__ void __launch_bounds__(512) k_walk_dc(WalkArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NP = 32 * NPL;
@@ -662,7 +665,7 @@ __global__ void __launch_bounds__(512) k_walk_dc(WalkArgs a) {
         const M128 m = a.cur[idx];
         uint64_t v = 0;
         if constexpr (NARROW) {
-            if (!dc_cell<NPL, false, T>(Lsm, bufs, roff, K, N, m, lane, a, st, a.limV, a.limL, v)) {
+            if (!dc_cell<NPL, false, T, VSAFE>(Lsm, bufs, roff, K, N, m, lane, a, st, a.limV, a.limL, v)) {
                 if (lane == 0) {
                     const unsigned long long pos = atomicAdd(a.ovfl_cnt, 1ull);
                     if (pos < a.ovfl_cap) a.ovfl[pos] = m;
@@ -837,14 +840,15 @@ static int walk_npl(const walk::WalkArgs &a, int grid, size_t smem, int *fused) 
         const int nw = lb + pw > budget ? 0 : (int)std::min<size_t>(16, (budget - lb) / pw);
         if (nw >= 2) {
             const size_t dsmem = lb + (size_t)nw * pw;
-            cudaError_t e = cudaFuncSetAttribute((const void *)walk::k_walk_dc<NPL, int32_t>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+            auto kern = a.vsafe ? walk::k_walk_dc<NPL, int32_t, true> : walk::k_walk_dc<NPL, int32_t, false>;
+            cudaError_t e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)dsmem);
             if (e != cudaSuccess) return (int)e;
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             const int per_sm = std::max<int>(1, (int)((228 * 1024) / (dsmem + 1024)));
-            walk::k_walk_dc<NPL, int32_t><<<sms * per_sm, nw * 32, dsmem, (cudaStream_t)a.stream>>>(a);
+            kern<<<sms * per_sm, nw * 32, dsmem, (cudaStream_t)a.stream>>>(a);
             *fused = 2;
             return (int)cudaGetLastError();
         }
@@ -879,9 +883,10 @@ int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, 
                 unsigned long long *next_cnt, void *table, uint64_t cap, unsigned long long *counter,
                 unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL,
                 unsigned long long *vol, int *fused, uint8_t *tags, unsigned tag, uint64_t next_cap,
-                int narrow, void *ovfl, unsigned long long *ovfl_cnt, uint64_t ovfl_cap) {
+                int narrow, void *ovfl, unsigned long long *ovfl_cnt, uint64_t ovfl_cap, int vsafe) {
     walk::WalkArgs a;
     a.narrow = narrow;
+    a.vsafe = vsafe;
     a.ovfl = (walk::M128 *)ovfl;
     a.ovfl_cnt = ovfl_cnt;
     a.ovfl_cap = ovfl_cap;
