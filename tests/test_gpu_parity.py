@@ -433,3 +433,37 @@ def test_front_end_at_scale_table2():
                 A[i][m - 1] = A[i][0] - 2 * A[i][1]
         assert B.dimension_modp(A) == analyze(A)["dim"]
 
+
+
+def test_cells_are_delaunay_for_paraboloid_lifting():
+    # The emitted cell list under the lifting w(p) = |p|^2 is
+    # the Delaunay triangulation (lower faces of the lifted points),
+    # checked against qhull (scipy) — independent of both the kernel and the
+    # oracle — at sizes that span several work items (N up to 60).
+    spatial = pytest.importorskip("scipy.spatial")
+    checked = 0
+    for seed in range(60):
+        d = 2 + seed % 2
+        n = 40 + seed % 21 if d == 2 else 24 + seed % 13
+        lo, hi = (-20, 20) if d == 2 else (-8, 8)
+        pts, _ = W.random_point_set(9100 + seed, d, n, lo, hi)
+        pts = list(dict.fromkeys(pts))
+        V = [(1,) + p for p in pts]
+        w = [sum(x * x for x in p) for p in pts]
+        tri = spatial.Delaunay(pts)
+        if len(tri.coplanar):
+            continue
+        plan = B.Plan.from_points(V, w)
+        try:
+            r = plan.degree()
+        except B.BdegError as e:
+            if e.status == B.bdeg.BDEG_E_DEGENERATE:     # cospherical points: ties
+                continue
+            raise
+        want = sorted(tuple(sorted(int(i) for i in s)) for s in tri.simplices)
+        got = plan.cells()
+        assert [c for c, _ in got] == want, seed
+        assert r.cells == len(want) and r.ties == 0
+        assert r.degree == sum(v for _, v in got)
+        checked += 1
+    assert checked >= 20, checked

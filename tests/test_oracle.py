@@ -393,3 +393,63 @@ def test_cell_list_is_a_subdivision():
         assert all(v >= 1 for _, v in cells)
         assert sum(v for _, v in cells) == nvol_pulling(pts)
         assert len(cells) == enumerate_lifted(d + 1, V, w)["cells"]
+
+
+def _delaunay_case(seed, d, n, lo, hi):
+    """Distinct random integer points with the paraboloid lifting |p|^2: the
+    lower faces of the lifted set project to the Delaunay triangulation
+    (the regular subdivision of Def. 1, for this lifting)."""
+    pts, _ = W.random_point_set(seed, d, n, lo, hi)
+    pts = list(dict.fromkeys(pts))
+    w = [sum(x * x for x in p) for p in pts]
+    return pts, [(1,) + p for p in pts], w
+
+
+def _on_hull_boundary(pts):
+    # brute force in the plane: p is on the boundary of conv(pts) iff some
+    # line through p and another point q leaves every point on one side
+    out = 0
+    for i, p in enumerate(pts):
+        for j, q in enumerate(pts):
+            if i == j:
+                continue
+            s = [(q[0] - p[0]) * (r[1] - p[1]) - (q[1] - p[1]) * (r[0] - p[0]) for r in pts]
+            if all(x >= 0 for x in s) or all(x <= 0 for x in s):
+                out += 1
+                break
+    return out
+
+
+def test_cells_are_delaunay_for_paraboloid_lifting():
+    # Independent pin of the oracle's cell LIST (not only its volume sum):
+    # with the lifting w(p) = |p|^2 the regular subdivision is the Delaunay
+    # triangulation, computed here by qhull (scipy), which shares nothing with
+    # the lower-face test of P:782-792.  In the plane every point is a vertex,
+    # so Euler's formula fixes the count: #triangles = 2n - b - 2 (b = points
+    # on the hull boundary).  Seeds with cospherical points (ties) are skipped.
+    spatial = pytest.importorskip("scipy.spatial")
+    from oracle import cell_list
+    checked = {2: 0, 3: 0}
+    for seed in range(200):
+        d = 2 + seed % 2
+        n = (12 + seed % 7) if d == 2 else (9 + seed % 5)
+        pts, V, w = _delaunay_case(7000 + seed, d, n, -6 if d == 2 else -4, 6 if d == 2 else 4)
+        if rank_fraction([[p[t] - pts[0][t] for t in range(d)] for p in pts]) < d:
+            continue
+        if enumerate_lifted(d + 1, V, w)["ties"]:
+            continue
+        tri = spatial.Delaunay(pts)
+        if len(tri.coplanar):
+            continue
+        want = sorted(tuple(sorted(int(i) for i in s)) for s in tri.simplices)
+        got = cell_list(d + 1, V, w)
+        assert [c for c, _ in got] == want, (seed, pts)
+        for c, v in got:                     # NVol = d! * Euclidean volume
+            assert v == abs(round(det_fraction([list(V[i]) for i in c])))
+        if d == 2:
+            assert len(got) == 2 * len(pts) - _on_hull_boundary(pts) - 2
+        assert sum(v for _, v in got) == nvol_pulling(pts)
+        checked[d] += 1
+        if min(checked.values()) >= 15:
+            break
+    assert checked[2] >= 15 and checked[3] >= 15, checked
