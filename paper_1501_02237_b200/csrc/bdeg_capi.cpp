@@ -136,42 +136,59 @@ uint64_t block_of(const bdeg_plan_s *p, uint64_t rank) {
 // V rows and of the lift row along sampled prefixes, as the kernel computes
 // them — steers the choice of the starting tier only (the kernel checks every
 // stored value against its tier's bounds and re-runs offending blocks).
+// One sampled elimination order (perm) in the integer type T; returns false
+// when a product leaves T (the caller retries in the wider type, or gives up).
+template <typename T>
+bool sample_one(const bdeg_plan_s *p, const std::vector<int> &perm, i128 &mv, i128 &ml) {
+    const int K = p->K, N = p->N;
+    std::vector<T> M((size_t)(K + 1) * N);          // row i, column l at M[i*N + l]
+    for (int l = 0; l < N; ++l) {
+        for (int i = 0; i < K; ++i) M[(size_t)i * N + l] = p->V[(size_t)l * K + i];
+        M[(size_t)K * N + l] = p->w[l];
+    }
+    std::vector<char> alive(K, 1);
+    T prev = 1;
+    T lv = 0, ll = 0;
+    for (int t = 0; t < K - 1; ++t) {
+        const int piv_c = perm[t];
+        int r = -1;
+        for (int i = 0; i < K; ++i) if (alive[i] && M[(size_t)i * N + piv_c] != 0) { r = i; break; }
+        if (r < 0) break;
+        const T piv = M[(size_t)r * N + piv_c];
+        for (int i = 0; i <= K; ++i) {
+            if (i == r || (i < K && !alive[i])) continue;
+            T *row = &M[(size_t)i * N];
+            const T *prow = &M[(size_t)r * N];
+            const T ci = row[piv_c];
+            for (int l = 0; l < N; ++l) {
+                T a, b2, num;
+                if (__builtin_mul_overflow(piv, row[l], &a) || __builtin_mul_overflow(ci, prow[l], &b2) ||
+                    __builtin_sub_overflow(a, b2, &num) || (sizeof(T) == 8 && num == (T)INT64_MIN))
+                    return false;
+                row[l] = num / prev;                 // exact (Sylvester)
+                const T v = row[l] < 0 ? -row[l] : row[l];
+                if (i < K) { if (v > lv) lv = v; } else { if (v > ll) ll = v; }
+            }
+        }
+        alive[r] = 0;
+        prev = piv;
+    }
+    if ((i128)lv > mv) mv = lv;
+    if ((i128)ll > ml) ml = ll;
+    return true;
+}
+
 void sample_bits(const bdeg_plan_s *p, int &bv, int &bl) {
     const int K = p->K, N = p->N;
     SplitMix64 g(0x5eed ^ p->seed_used);
     i128 mv = 1, ml = 1;
     bool big = false;
+    std::vector<int> perm(N);
     for (int s = 0; s < 32 && !big; ++s) {
-        std::vector<int> perm(N);
         for (int i = 0; i < N; ++i) perm[i] = i;
         for (int i = N - 1; i > 0; --i) std::swap(perm[i], perm[g.next() % (uint64_t)(i + 1)]);
-        std::vector<std::vector<i128>> M(K + 1, std::vector<i128>(N));
-        for (int l = 0; l < N; ++l) {
-            for (int i = 0; i < K; ++i) M[i][l] = p->V[(size_t)l * K + i];
-            M[K][l] = p->w[l];
-        }
-        std::vector<char> alive(K, 1);
-        i128 prev = 1;
-        for (int t = 0; t < K - 1 && !big; ++t) {
-            const int piv_c = perm[t];
-            int r = -1;
-            for (int i = 0; i < K; ++i) if (alive[i] && M[i][piv_c] != 0) { r = i; break; }
-            if (r < 0) break;
-            const i128 piv = M[r][piv_c];
-            for (int i = 0; i <= K && !big; ++i) {
-                if (i == r || (i < K && !alive[i])) continue;
-                const i128 ci = M[i][piv_c];
-                for (int l = 0; l < N; ++l) {
-                    i128 a, b2;
-                    if (__builtin_mul_overflow(piv, M[i][l], &a) || __builtin_mul_overflow(ci, M[r][l], &b2)) { big = true; break; }
-                    M[i][l] = (a - b2) / prev;
-                    const i128 v = M[i][l] < 0 ? -M[i][l] : M[i][l];
-                    if (i < K) { if (v > mv) mv = v; } else { if (v > ml) ml = v; }
-                }
-            }
-            alive[r] = 0;
-            prev = piv;
-        }
+        // int64 first (C5, master spaces), checked int128 when a product leaves it
+        if (!sample_one<int64_t>(p, perm, mv, ml) && !sample_one<i128>(p, perm, mv, ml)) big = true;
     }
     auto nbits = [](i128 x) { int b = 0; while (x > 0) { ++b; x >>= 1; } return b; };
     bv = big ? 127 : nbits(mv);
