@@ -136,6 +136,22 @@ uint64_t block_of(const bdeg_plan_s *p, uint64_t rank) {
 // V rows and of the lift row along sampled prefixes, as the kernel computes
 // them — steers the choice of the starting tier only (the kernel checks every
 // stored value against its tier's bounds and re-runs offending blocks).
+// Exact division by d != 0 (the quotient is known to be an integer): in int64
+// shift out d's 2-adic part and multiply by the odd part's inverse mod 2^64
+// (Newton); int128 divides.
+inline uint64_t odd_inverse(int64_t d, int &tz) {
+    tz = __builtin_ctzll((uint64_t)d);
+    const uint64_t o = (uint64_t)(d >> tz);          // odd part (arithmetic shift keeps the sign)
+    uint64_t x = o;                                  // correct to 3 bits
+    for (int i = 0; i < 5; ++i) x *= 2 - o * x;
+    return x;
+}
+inline uint64_t odd_inverse(i128, int &tz) { tz = 0; return 0; }
+inline int64_t exact_div(int64_t n, int64_t, uint64_t inv, int tz) {
+    return (int64_t)((uint64_t)(n >> tz) * inv);
+}
+inline i128 exact_div(i128 n, i128 d, uint64_t, int) { return n / d; }
+
 // One sampled elimination order (perm) in the integer type T; returns false
 // when a product leaves T (the caller retries in the wider type, or gives up).
 template <typename T>
@@ -155,6 +171,8 @@ bool sample_one(const bdeg_plan_s *p, const std::vector<int> &perm, i128 &mv, i1
         for (int i = 0; i < K; ++i) if (alive[i] && M[(size_t)i * N + piv_c] != 0) { r = i; break; }
         if (r < 0) break;
         const T piv = M[(size_t)r * N + piv_c];
+        int dtz = 0;
+        const uint64_t dinv = odd_inverse(prev, dtz);
         for (int i = 0; i <= K; ++i) {
             if (i == r || (i < K && !alive[i])) continue;
             T *row = &M[(size_t)i * N];
@@ -165,7 +183,7 @@ bool sample_one(const bdeg_plan_s *p, const std::vector<int> &perm, i128 &mv, i1
                 if (__builtin_mul_overflow(piv, row[l], &a) || __builtin_mul_overflow(ci, prow[l], &b2) ||
                     __builtin_sub_overflow(a, b2, &num) || (sizeof(T) == 8 && num == (T)INT64_MIN))
                     return false;
-                row[l] = num / prev;                 // exact (Sylvester)
+                row[l] = exact_div(num, prev, dinv, dtz);   // exact (Sylvester)
                 const T v = row[l] < 0 ? -row[l] : row[l];
                 if (i < K) { if (v > lv) lv = v; } else { if (v > ll) ll = v; }
             }
