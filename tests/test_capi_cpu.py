@@ -167,3 +167,22 @@ def test_cell_normal_matches_oracle_solve():
         assert p.cell_normal(cell) == h
         done += 1
     assert done > 20
+
+
+def test_planner_tier_follows_value_sizes():
+    # host planner (DESIGN.md §3 "Arithmetic tiers"): sampled elimination
+    # values of <= 28 bits start in tier 0, a wide lift row with narrow V rows
+    # in tier 1, and V coordinates ~2^20 with a 2^50 lifting (products beyond
+    # int64: the sampler's int128 retry) in tier 2
+    import random
+
+    def tier(K, N, cv, lw, seed=1):
+        r = random.Random(seed)
+        V = [(1,) + tuple(r.randint(-cv, cv) for _ in range(K - 1)) for _ in range(N)]
+        w = [r.randint(0, lw) for _ in range(N)]
+        with B.Plan.from_points(V, w) as p:
+            return p.info().tier
+
+    assert tier(4, 12, 2, 1 << 10) == 0
+    assert tier(4, 12, 2, 1 << 40) == 1
+    assert tier(6, 14, 1 << 20, 1 << 50) == 2
