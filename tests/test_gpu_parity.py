@@ -467,3 +467,21 @@ def test_cells_are_delaunay_for_paraboloid_lifting():
         assert r.degree == sum(v for _, v in got)
         checked += 1
     assert checked >= 20, checked
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_auto_tier2_wide_values_match_oracle(seed):
+    # planner-chosen tier 2 (int64 values, checked int128 products; DESIGN.md
+    # §3) on V-minors of ~2^39 and lift minors of ~2^51, bit-exact vs the oracle
+    r = random.Random(seed)
+    K, N = 4, 16
+    V = [(1,) + tuple(r.randint(-(1 << 12), 1 << 12) for _ in range(K - 1)) for _ in range(N)]
+    w = [r.randint(0, 1 << 24) for _ in range(N)]
+    plan = B.Plan.from_points(V, w)
+    assert plan.info().tier == 2
+    got = plan.degree()
+    want = enumerate_lifted(K, V, w)
+    assert (got.degree, got.cells, got.singular, got.ties) == \
+        (want["volume"], want["cells"], want["singular"], want["ties"])
+    from oracle import cell_list
+    assert plan.cells() == cell_list(K, V, w)
