@@ -3,7 +3,7 @@
 configuration — BASELINE.json configs[4], "k=8 over 40 lifted lattice points
 (~7.7e7 candidate simplices), rank space sharded across 8xB200".
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|w26|w34|w27|w24]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|w<m><k>] [--degree-only]
   python bench.py --impl reference ...        # the CPU oracle arm
 
 A step = one pass of the whole hot path over the full rank space: the
@@ -38,23 +38,65 @@ METRIC = "simplices/sec and time-to-degree at 1/2/4/8 B200; % integer-pipe peak"
 UNIT = "simplices/s"
 
 
-def workload(name):
-    """-> (description, K, V point-major, lifting, extra config dict)."""
-    import workloads as W
-    if name == "c5":
-        V, w = W.c5_points(1)
-        return ("C5 synthetic: K=8 vectors (1,a), a uniform in [-3,3]^7, N=40 distinct points, "
-                "lifting uniform in [0,2^20) (SplitMix64 seed 1)", 8, V, w, {"seed": 1})
-    if not (name.startswith("w") and len(name) == 3 and name[1:].isdigit()):
-        raise SystemExit(f"unknown workload {name!r} (c5 or w<m><k>)")
-    m, k = int(name[1]), int(name[2])
-    from oracle import point_configuration  # input preparation only (front end of the oracle)
-    A, b = W.master_space_system(m, k)
-    lift = W.liftings(len(A) + 1, 1)
-    cfg = point_configuration(A, b, lift)
-    K, V, w = cfg["cone"]
-    return (f"master space grad W_{{{m},{k}}} (PAPER.md Table 3), lifted point configuration "
-            f"K={K}, N={len(V)}", K, V, w, {"m": m, "k": k, "seed": 1})
+class Workload:
+    """A bench workload as the user hands it to the library: a lifted point
+    configuration (C5, `bdeg_plan_points`) or a binomial system x^A = b
+    (W_{m,k}, `bdeg_plan`: the library's own SNF / P_0 / LLL front end)."""
+
+    def __init__(self, name):
+        import workloads as W
+        self.name = name
+        if name == "c5":
+            self.kind = "points"
+            self.V, self.w = W.c5_points(1)
+            self.desc = ("C5 synthetic: K=8 vectors (1,a), a uniform in [-3,3]^7, N=40 distinct points, "
+                         "lifting uniform in [0,2^20) (SplitMix64 seed 1)")
+            self.extra = {"seed": 1}
+        elif name.startswith("w") and len(name) == 3 and name[1:].isdigit():
+            self.kind = "system"
+            m, k = int(name[1]), int(name[2])
+            self.A, self.b = W.master_space_system(m, k)
+            self.lift = W.liftings(len(self.A) + 1, 1)
+            self.desc = (f"master space grad W_{{{m},{k}}} (PAPER.md Table 3): x^A = b through the "
+                         f"library's front end (n={len(self.A)} variables, m={len(self.A[0])} binomials)")
+            self.extra = {"m": m, "k": k, "seed": 1}
+        else:
+            raise SystemExit(f"unknown workload {name!r} (c5 or w<m><k>)")
+
+    def plan(self, **opts):
+        import paper_1501_02237_b200 as B
+        if self.kind == "points":
+            return B.Plan.from_points(self.V, self.w, **opts)
+        return B.Plan.from_system(self.A, self.b, self.lift, **opts)
+
+    def h2d_bytes(self, K, N):
+        """Bytes the public call uploads per step: the lifted matrix and the binomial table."""
+        return (((K + 1) * N * 8 + 15) // 16) * 16 + 65 * 34 * 8
+
+    def oracle_points(self):
+        """(K, V, w) for the CPU baseline only (the oracle's own front end)."""
+        if self.kind == "points":
+            return len(self.V[0]), self.V, self.w
+        from oracle import point_configuration  # cpu_baseline / reference arm only
+        K, V, w = point_configuration(self.A, self.b, self.lift)["cone"]
+        return K, V, w
+
+
+def workload_sizes(name):
+    """(K, N) of a workload without the GPU library: C5 directly; W_{m,k} via the
+    oracle's front end (the point count is basis-independent)."""
+    wl = Workload(name)
+    K, V, _ = wl.oracle_points()
+    return K, len(V)
+
+
+def bench_config(wl, K, N, world):
+    """ONE config dict, emitted identically by both arms."""
+    return {"workload": wl.desc, "K": K, "N": N, "candidates": math.comb(N, K),
+            "l2": "GPU arm: L2 flushed between steps (256 MiB write outside the timed events)",
+            "parallelism": f"rank space sharded over {world} GPU(s): static interleaved items, "
+                           "then a cross-GPU work-stealing tail; one all-reduce of 16 int64 slots",
+            **wl.extra}
 
 
 def load_peaks():
@@ -136,7 +178,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    desc, K, V, w, extra = workload(args.workload)
+    wl = Workload(args.workload)
+    K, V, w = wl.oracle_points()
     total = math.comb(len(V), K)
     # each step is a bounded sample; the whole --steps/--warmup run stays at
     # ~2.4e8 candidates (about 3 minutes of the oracle on 16 host cores)
@@ -156,13 +199,37 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * wall / max(1, args.steps),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int128",
         "data": "synthetic",
-        "config": {"workload": desc, "K": K, "N": len(V), "candidates": total, **extra},
+        "config": bench_config(wl, K, len(V), args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "time_to_degree_s_extrapolated": total / value,
     }
     print(json.dumps(line), flush=True)
+
+
+def algorithmic_ops_per_candidate(K, nonsingular_frac, tested=2.0):
+    """SURVEY §8.d 'Algorithmic work per candidate' (integer ops, an update
+    u = (a*b - c*d)/e counted as 4): Bareiss (K-1)K(2K-1)/6 updates; for
+    det != 0 the lift functional (K(K+1)/2 multiply-adds = 2 ops each, plus K
+    exact divisions) and the facet test (E[#tested] ~ 2 points x (K+1)
+    multiply-adds).  676 at K = 8 with no singular candidates."""
+    bareiss = 4.0 * (K - 1) * K * (2 * K - 1) / 6.0
+    lift = K * (K + 1) + K
+    facet = 2.0 * tested * (K + 1)
+    return bareiss + nonsingular_frac * (lift + facet)
+
+
+def load_int_peak():
+    """The measured integer issue peak (tools/intpipe_bench.cu on a B200):
+    lane-ops per SM clock, all integer pipes together and the ALU pipe alone."""
+    pth = os.path.join(ROOT, "profiles", "r2_intpipe_peaks.json")
+    if os.path.exists(pth):
+        d = json.load(open(pth))
+        alu = max(d[k]["lane_ops_per_clk_per_sm"] for k in ("iadd3", "lop3", "shf"))
+        allp = max(alu, d["imad"]["lane_ops_per_clk_per_sm"], d["imad_lop3_mix"]["lane_ops_per_clk_per_sm"])
+        return allp, alu, "measured (profiles/r2_intpipe_peaks.json)"
+    return 128.0, 64.0, "fallback: 4 SMSP x 32 lanes issue/clk/SM (not measured)"
 
 
 def run_gpu(args):
@@ -188,17 +255,19 @@ def run_gpu(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-    desc, K, V, w, extra = workload(args.workload)
-    total = math.comb(len(V), K)
+    wl = Workload(args.workload)
     stream = torch.cuda.current_stream()
+    flags = B.bdeg.FLAG_DEGREE_ONLY if args.degree_only else 0
 
-    plan = B.Plan.from_points(V, w, rank=rank, world=world, stream=stream.cuda_stream, device=local)
+    plan = wl.plan(rank=rank, world=world, stream=stream.cuda_stream, device=local, flags=flags)
     plan.use_torch_workspace(local)
+    info = plan.info()
+    K, N = info.K, info.N
+    total = math.comb(N, K)
     steal = world > 1 and os.environ.get("BDEG_STEAL", "1") == "1"
-    if steal:        # one global item queue over all GPUs (CUDA IPC + NVLink atomics)
+    if steal:        # static share first, then one global tail queue (CUDA IPC + NVLink atomics)
         from paper_1501_02237_b200.multi import enable_work_stealing
         enable_work_stealing(plan, local)
-    info = plan.info()
     slots = torch.zeros(B.NSLOTS, dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -240,9 +309,10 @@ def run_gpu(args):
     res = plan.finalize(slots.cpu().tolist())
     value = total / (ms_step / 1000.0)
 
-    # ---- e2e: the public C-ABI call with HOST buffers, every step
+    # ---- e2e: the public C-ABI call with HOST buffers, every step (planning
+    # from the host inputs incl. the front end, H2D, kernel, D2H of the slots)
     e2e_ms = []
-    h2d = (((K + 1) * len(V) * 8 + 15) // 16) * 16 + 65 * 34 * 8
+    h2d = wl.h2d_bytes(K, N)
     d2h = B.NSLOTS * 8
     e2e_steps = min(args.steps, 30)     # a plan per step: bounded to keep the run short
     for s in range(args.warmup + e2e_steps):
@@ -250,14 +320,12 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        with B.Plan.from_points(V, w, rank=rank, world=world, stream=stream.cuda_stream, device=local) as p2:
+        with wl.plan(rank=rank, world=world, stream=stream.cuda_stream, device=local, flags=flags) as p2:
             if world == 1:
                 r2 = p2.degree()
             else:
-                sl = torch.zeros(B.NSLOTS, dtype=torch.int64, device=dev)
-                p2.degree_partial(sl.data_ptr())
-                dist.all_reduce(sl, op=dist.ReduceOp.SUM)
-                r2 = p2.finalize(sl.cpu().tolist())
+                from paper_1501_02237_b200.multi import degree_distributed
+                r2 = degree_distributed(p2, dev)
         dt = (time.perf_counter() - t0) * 1000.0
         if s >= args.warmup:
             e2e_ms.append(dt)
@@ -269,7 +337,7 @@ def run_gpu(args):
 
     if rank == 0 and world > 1:
         # the combined shards must equal a single-GPU run over the whole rank space
-        with B.Plan.from_points(V, w, stream=stream.cuda_stream, device=local) as p1:
+        with wl.plan(stream=stream.cuda_stream, device=local, flags=flags) as p1:
             full = p1.degree()
         assert (full.degree, full.cells, full.candidates) == (res.degree, res.cells, res.candidates), \
             "multi-GPU combine differs from the single-GPU result"
@@ -277,25 +345,33 @@ def run_gpu(args):
         peaks, peak_kind = load_peaks()
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-        peak_ops = 128.0 * n_sm * sm_mhz * 1e6 * world         # 4 SMSP x 32 lanes issue / clk / SM
-        # algorithmic integer ops per step: 4 per
-        # fraction-free update (2 mul, 1 sub, 1 exact division) + 2 per
-        # point per leaf facet test (slope key, compare)
-        alg_ops = 4.0 * res.updates + 2.0 * res.leaves * len(V)
-        achieved = alg_ops / (ms_step / 1000.0)
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(args.workload)
-        # executed-instruction utilisation of the same kernel from the committed
-        # ncu --set full capture (the counter-backed side of the roofline)
+        lanes, alu_lanes, lanes_kind = load_int_peak()
+        peak_ops = lanes * n_sm * sm_mhz * 1e6 * world
+        t_s = ms_step / 1000.0
+        # (1) SURVEY §8.d's algorithmic integer ops per candidate (the headline frac)
+        nonsing = 1.0 - (res.singular / res.candidates if res.candidates and not args.degree_only else 0.0)
+        opc = algorithmic_ops_per_candidate(K, nonsing)
+        achieved = opc * total / t_s
+        # (2) the kernel's own work (its counters): 4 ops per fraction-free
+        # update + 2 per point per leaf facet test
+        own_ops = 4.0 * res.updates + 2.0 * res.leaves * N
+        # (3) executed instructions of the same kernel (committed ncu --set full capture)
         executed = None
         ep = os.path.join(ROOT, "profiles", "ncu_executed.json")
         if os.path.exists(ep):
             executed = json.load(open(ep)).get(args.workload)
+        exec_frac = None
+        if executed and executed.get("warp_inst_per_launch"):
+            thr = executed["warp_inst_per_launch"] * executed.get("threads_per_inst", 32.0)
+            exec_frac = thr / t_s / peak_ops
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(args.workload)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            v, cores, sample = cpu_oracle_sample(K, V, w, args.ref_sample)
+            Ko, Vo, wo = wl.oracle_points()
+            v, cores, sample = cpu_oracle_sample(Ko, Vo, wo, args.ref_sample)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -303,20 +379,24 @@ def run_gpu(args):
             "scaling": "strong", "vs_baseline": None,
             "dtype": B.bdeg.TIER_DTYPE[info.tier],
             "data": "synthetic",
-            "config": {"workload": desc, "K": K, "N": len(V), "candidates": total,
-                       "l2": "flushed between steps (256 MiB write outside the timed events)",
-                       "inner_levels": info.inner_levels, "tier": info.tier,
-                       "parallelism": (f"rank-space work items from one cross-GPU queue (IPC, NVLink atomics) over {world} GPUs"
-                                       if steal else f"rank-space work items interleaved over {world} GPU(s)"), **extra},
+            "config": bench_config(wl, K, N, world),
+            "kernel": {"inner_levels": info.inner_levels, "tier": info.tier, "work_items": plan.num_items(),
+                       "degree_only": bool(args.degree_only), "work_stealing_tail": steal},
             "time_to_degree_ms": e2e_step,
             "result": {"degree": res.degree, "cells": res.cells, "singular": res.singular,
                        "candidates": res.candidates, "ties": res.ties,
                        "overflow_reruns": res.overflow_reruns, "leaves": res.leaves},
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
                          "unit": "Tintop/s", "frac": achieved / peak_ops, "traffic": traffic,
-                         "peak_basis": f"128 int lane-ops/clk/SM x {n_sm} SMs x {sm_mhz:.0f} MHz "
-                                       f"({peak_kind} sm_max_mhz) x {world} GPU(s)",
-                         "algorithmic_ops_per_step": alg_ops, "ncu_executed": executed},
+                         "peak_basis": f"{lanes:.1f} integer lane-ops/clk/SM ({lanes_kind}) x {n_sm} SMs x "
+                                       f"{sm_mhz:.0f} MHz ({peak_kind} sm_max_mhz) x {world} GPU(s)",
+                         "algorithmic_ops_per_candidate": opc,
+                         "fractions": {
+                             "algorithmic_8d": achieved / peak_ops,
+                             "own_work": own_ops / t_s / peak_ops,
+                             "ncu_executed": exec_frac,
+                             "alu_pipe_only_algorithmic": achieved / (alu_lanes * n_sm * sm_mhz * 1e6 * world)},
+                         "ncu_executed": executed},
             "cpu_baseline": cpu,
             "e2e": {"value": total / (e2e_step / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -340,6 +420,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=4_000_000,
                     help="candidates per oracle sample (cpu_baseline / reference arm)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--degree-only", action="store_true",
+                    help="skip cell-dead subtrees (singular becomes a lower bound)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

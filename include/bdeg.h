@@ -134,6 +134,14 @@ bdeg_status bdeg_plan_points(int32_t K, int32_t N, const int64_t *V, const int64
 /* Front-end fields of the result (no device work). */
 bdeg_status bdeg_plan_info(bdeg_plan_t plan, bdeg_result *out);
 
+/* The lifted configuration the plan currently enumerates (host copies): V
+ * (N*K int64, POINT-major, bdeg_plan_info's point order: distinct non-zero
+ * columns of P_0 in variable order, then the origin unless homogeneous —
+ * Prop. 4) and omega (N int64: the lifting in use after any
+ * bdeg_relift, and for N > 64 the basis-seeded lifting).  Either
+ * pointer may be NULL.  BDEG_E_INVALID for a d = 0 plan (no points). */
+bdeg_status bdeg_plan_points_get(bdeg_plan_t plan, int64_t *V, int64_t *omega);
+
 /* Device workspace: bytes needed, and an optional caller-owned device buffer
  * (e.g. a torch.uint8 CUDA tensor) that must outlive the plan's device work.
  * Without it the plan allocates with cudaMalloc on first use. */

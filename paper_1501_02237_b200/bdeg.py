@@ -84,7 +84,8 @@ EXPORTS = ["bdeg_default_options", "bdeg_plan", "bdeg_plan_points", "bdeg_plan_i
            "bdeg_degree_partial", "bdeg_finalize", "bdeg_relift", "bdeg_last_error",
            "bdeg_status_str", "bdeg_destroy", "bdeg_launch_count", "bdeg_num_items",
            "bdeg_item_range", "bdeg_cells", "bdeg_degree_walk", "bdeg_cell_normal",
-           "bdeg_steal_create", "bdeg_steal_attach", "bdeg_rank_modp", "bdeg_dimension_modp"]
+           "bdeg_steal_create", "bdeg_steal_attach", "bdeg_rank_modp", "bdeg_dimension_modp",
+           "bdeg_plan_points_get"]
 
 
 def _load():
@@ -100,6 +101,7 @@ def _load():
     lib.bdeg_plan_points.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int64),
                                      P(ctypes.c_int64), P(_Options), P(plan_t)]
     lib.bdeg_plan_info.argtypes = [plan_t, P(_Result)]
+    lib.bdeg_plan_points_get.argtypes = [plan_t, P(ctypes.c_int64), P(ctypes.c_int64)]
     lib.bdeg_workspace_bytes.argtypes = [plan_t]
     lib.bdeg_workspace_bytes.restype = ctypes.c_size_t
     lib.bdeg_set_workspace.argtypes = [plan_t, ctypes.c_void_p, ctypes.c_size_t]
@@ -138,7 +140,7 @@ def _load():
     lib.bdeg_dimension_modp.restype = ctypes.c_int
     lib.bdeg_launch_count.argtypes = []
     lib.bdeg_launch_count.restype = ctypes.c_uint64
-    for name in ["bdeg_plan", "bdeg_plan_points", "bdeg_plan_info", "bdeg_set_workspace",
+    for name in ["bdeg_plan", "bdeg_plan_points", "bdeg_plan_info", "bdeg_plan_points_get", "bdeg_set_workspace",
                  "bdeg_degree", "bdeg_degree_range", "bdeg_degree_partial", "bdeg_finalize",
                  "bdeg_relift"]:
         getattr(lib, name).restype = ctypes.c_int
@@ -321,6 +323,16 @@ class Plan:
         r = _Result()
         _check(lib.bdeg_plan_info(self._h, ctypes.byref(r)), self._h)
         return _result(r)
+
+    def points(self):
+        """(K, V point-major as tuples, lifting) the plan enumerates (bdeg_plan_points_get)."""
+        info = self.info()
+        K, N = info.K, info.N
+        Vb = (ctypes.c_int64 * max(1, K * N))()
+        wb = (ctypes.c_int64 * max(1, N))()
+        _check(lib.bdeg_plan_points_get(self._h, Vb, wb), self._h)
+        V = [tuple(Vb[l * K + i] for i in range(K)) for l in range(N)]
+        return K, V, [wb[l] for l in range(N)]
 
     def num_items(self) -> int:
         return int(lib.bdeg_num_items(self._h))

@@ -221,6 +221,17 @@ void sample_bits(const bdeg_plan_s *p, int &bv, int &bl) {
     }
 }
 
+// A narrow tier (forced by a flag, or chosen before a re-lift) still needs
+// the RAW values inside its bounds: the shared-memory prefix multiplies them
+// in int64 before any range check, and the narrow walk stores them as int32.
+void raw_tier_bounds(bdeg_plan_s *p) {
+    int64_t mv = 0, mw = 0;
+    for (int64_t v : p->V) mv = std::max(mv, v < 0 ? -v : v);
+    for (int64_t v : p->w) mw = std::max(mw, v < 0 ? -v : v);
+    if (p->tier == 0 && (mv >= INT32_MAX || mw >= INT32_MAX)) p->tier = 1;
+    if (p->tier == 1 && (mv >= ((int64_t)1 << p->bits_v) || mw >= ((int64_t)1 << p->bits_l))) p->tier = 2;
+}
+
 void choose_tier_and_blocks(bdeg_plan_s *p) {
     p->total = C(p->binom, p->N, p->K);
     int bv = 0, bl = 0;
@@ -254,6 +265,7 @@ void choose_tier_and_blocks(bdeg_plan_s *p) {
     if (p->opt.flags & BDEG_FLAG_FORCE_TIER0) p->tier = 0;
     if (p->opt.flags & BDEG_FLAG_FORCE_TIER1) p->tier = 1;
     if (p->opt.flags & BDEG_FLAG_FORCE_TIER2) p->tier = 2;
+    raw_tier_bounds(p);
     // Register-DFS depth S (deep: the DFS does one fraction-free step per
     // tree node), smem prefix T = K-1-S, and the work-item depth D >= T chosen
     // so that the largest item C(N-D, K-D) is a small fraction of the
@@ -341,13 +353,19 @@ bdeg_status finish_plan(bdeg_plan_s *p) {
         p->bits_v = std::min(30, std::max(bv + 2, 8));
         p->bits_l = 61 - p->bits_v;
         p->tier = (bv <= 28 && bl <= 28) ? 0 : ((bv + 2 <= 30 && bl < p->bits_l) ? 1 : 2);
+        if (p->opt.flags & BDEG_FLAG_FORCE_TIER0) p->tier = 0;
+        if (p->opt.flags & BDEG_FLAG_FORCE_TIER1) p->tier = 1;
+        if (p->opt.flags & BDEG_FLAG_FORCE_TIER2) p->tier = 2;
         p->total = 0;
         p->S = p->T = p->D = 0;
         p->nblocks = 0;
         seed_basis_lifting(p);
+        raw_tier_bounds(p);
     } else {
         choose_tier_and_blocks(p);
     }
+    // one re-run queue entry per work item: the queue cannot be exhausted
+    p->ovf_cap = std::max<uint64_t>(1, p->nblocks);
     p->l_dirty = true;
     return BDEG_OK;
 }
@@ -363,11 +381,15 @@ void rebuild_points(bdeg_plan_s *p) {
 // cudaGetDeviceProperties / cudaMalloc / cudaFree every time.
 struct DevInfo { bool ok = false; int sms = 0, major = 0; };
 std::mutex g_mu;
-DevInfo g_dev[64];
-std::vector<std::pair<size_t, void *>> g_pool[64];
+constexpr int kMaxDevices = 64;
+DevInfo g_dev[kMaxDevices];
+std::vector<std::pair<size_t, void *>> g_pool[kMaxDevices];
 std::map<std::string, void *> g_steal_local;   // IPC handles exported by this process
 
+DevInfo g_dev_none;
+
 const DevInfo &dev_info(int d) {
+    if (d < 0 || d >= kMaxDevices) return g_dev_none;   // ok = false
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_dev[d].ok) {
         cudaDeviceProp prop;
@@ -381,7 +403,7 @@ const DevInfo &dev_info(int d) {
 }
 
 void *pool_get(int d, size_t bytes, size_t *got) {
-    {
+    if (d >= 0 && d < kMaxDevices) {
         std::lock_guard<std::mutex> lk(g_mu);
         auto &v = g_pool[d];
         for (size_t i = 0; i < v.size(); ++i)
@@ -399,6 +421,7 @@ void *pool_get(int d, size_t bytes, size_t *got) {
 }
 
 void pool_put(int d, void *ptr, size_t bytes) {
+    if (d < 0 || d >= kMaxDevices) { cudaFree(ptr); return; }
     std::lock_guard<std::mutex> lk(g_mu);
     auto &v = g_pool[d];
     if (v.size() < 8) v.push_back({bytes, ptr});
@@ -407,6 +430,8 @@ void pool_put(int d, void *ptr, size_t bytes) {
 
 bdeg_status ensure_device(bdeg_plan_s *p) {
     cudaError_t e;
+    if (p->opt.device < 0 || p->opt.device >= kMaxDevices)
+        return fail(p, BDEG_E_INVALID, "device ordinal out of range");
     if (p->dev_ready || p->opt.device >= 0) {
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= p->opt.device)
@@ -441,8 +466,8 @@ bdeg_status ensure_device(bdeg_plan_s *p) {
         if ((e = cudaMemcpyAsync(p->d_B, p->binom.data(), p->binom.size() * 8, cudaMemcpyHostToDevice, st)) !=
             cudaSuccess)
             return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
-        cudaEventCreate(&p->ev0);
-        cudaEventCreate(&p->ev1);
+        if ((e = cudaEventCreate(&p->ev0)) != cudaSuccess || (e = cudaEventCreate(&p->ev1)) != cudaSuccess)
+            return fail(p, BDEG_E_CUDA, std::string("cudaEventCreate: ") + cudaGetErrorString(e));
         LaunchArgs a{};
         a.P.K = p->K; a.P.N = p->N; a.P.S = p->S; a.P.T = p->T;
         a.tier = p->tier;
@@ -618,12 +643,21 @@ bdeg_status cells_range(bdeg_plan_s *p, uint64_t b, uint64_t e, uint64_t *h_out,
     s = enqueue_range(p, b, e, p->d_slots, 0, 1, 2, buf.u(), cnt.u(), cap, first_cell_search);
     if (s) return s;
     uint64_t n = 0;
+    int64_t h[kNSlots];
     cudaMemcpyAsync(&n, cnt.p, 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h, p->d_slots, kNSlots * 8, cudaMemcpyDeviceToHost, st);
     cudaError_t ce = cudaStreamSynchronize(st);
     if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
+    // tier 2 only (no replay): an item whose values left int64 dropped its cells
+    if (h[SLOT_FATAL] > 0)
+        return fail(p, BDEG_E_TOO_LARGE, "cell emission: an exact elimination value exceeded the int64 tier");
+    // a would-be cell on a tie: the lifting is not generic, the list is not a subdivision
+    if (h[SLOT_TIES] > 0)
+        return fail(p, BDEG_E_DEGENERATE, "degenerate lifting: a would-be cell has a zero facet value");
     const uint64_t m = std::min(n, cap);
     if (m && h_out) {
-        ce = cudaMemcpy(h_out, buf.p, m * 16, cudaMemcpyDeviceToHost);
+        ce = cudaMemcpyAsync(h_out, buf.p, m * 16, cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
         if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
     }
     *count = n;
@@ -1031,6 +1065,14 @@ bdeg_status bdeg_plan_info(bdeg_plan_t p, bdeg_result *out) {
     return BDEG_OK;
 }
 
+bdeg_status bdeg_plan_points_get(bdeg_plan_t p, int64_t *V, int64_t *omega) {
+    if (!p) return fail(p, BDEG_E_INVALID, "NULL plan");
+    if (p->K == 0) return fail(p, BDEG_E_INVALID, "d = 0: the plan has no point configuration");
+    if (V) std::memcpy(V, p->V.data(), p->V.size() * sizeof(int64_t));
+    if (omega) std::memcpy(omega, p->w.data(), p->w.size() * sizeof(int64_t));
+    return BDEG_OK;
+}
+
 size_t bdeg_workspace_bytes(bdeg_plan_t p) { return p && p->K > 0 ? layout(p).total : 0; }
 
 bdeg_status bdeg_set_workspace(bdeg_plan_t p, void *d_ptr, size_t bytes) {
@@ -1053,6 +1095,7 @@ bdeg_status bdeg_relift(bdeg_plan_t p, int32_t attempt) {
     if (p->points_mode) p->w = p->lift;
     else rebuild_points(p);
     seed_basis_lifting(p);
+    raw_tier_bounds(p);
     p->relifts = attempt;
     p->l_dirty = true;
     return BDEG_OK;
@@ -1135,10 +1178,18 @@ bdeg_status bdeg_finalize(bdeg_plan_t p, const int64_t *h_slots, bdeg_result *ou
         *out = r;
         return BDEG_OK;
     }
+    // the re-run queue holds one entry per work item, so it cannot be exhausted
     if (h_slots[SLOT_QFULL] > 0)
-        return fail(p, BDEG_E_TOO_LARGE, "overflow re-run queue exhausted; rerun with BDEG_FLAG_FORCE_TIER2");
+        return fail(p, BDEG_E_TOO_LARGE, "overflow re-run queue exhausted (internal error)");
     bdeg_status s = slots_to_result(p, h_slots, &r);
     if (s) return s;
+    // a would-be cell with a zero facet value on any rank: the lifting is not
+    // generic, the summed volume is not a degree.  Every rank must
+    // re-lift with the same attempt (bdeg_relift) and recompute (multi.py).
+    if (r.ties > 0)
+        return fail(p, BDEG_E_DEGENERATE,
+                    p->user_lift ? "degenerate user lifting: a would-be cell has a zero facet value"
+                                 : "degenerate generated lifting: call bdeg_relift(attempt+1) on every rank and recompute");
     *out = r;
     return BDEG_OK;
 }
@@ -1333,6 +1384,9 @@ const char *bdeg_status_str(bdeg_status s) {
 
 void bdeg_destroy(bdeg_plan_t p) {
     if (!p) return;
+    // bdeg_degree_partial is asynchronous: the plan's kernels may still read
+    // the workspace, which the pool may hand to the next plan
+    if (p->dev_ready) cudaStreamSynchronize((cudaStream_t)p->opt.stream);
     if (p->own_ws && p->ws) pool_put(p->opt.device, p->ws, p->ws_bytes);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);

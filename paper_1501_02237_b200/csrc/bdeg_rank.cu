@@ -42,6 +42,9 @@ __global__ void k_eliminate(uint32_t *M, int n, int m, int r, int j, uint32_t p,
     for (int i = r + 1 + blockIdx.x; i < n; i += gridDim.x) {
         uint32_t *row = M + (size_t)i * m;
         const uint32_t a = row[j];
+        // every thread has read the pivot-column entry before any thread of
+        // the block overwrites it (t == j below); `a` is block-uniform
+        __syncthreads();
         if (a == 0) continue;
         const uint32_t f = mulmod(a, inv_piv, p);
         const uint32_t *prow = M + (size_t)r * m;

@@ -1,15 +1,22 @@
 """Multi-GPU combine (one process per GPU, torch.distributed as plumbing).
 
-Each rank runs bdeg_degree_partial over its interleaved share of the work
-items into a 16-slot int64 device buffer; one all-reduce(SUM) over NCCL
-(NVLink/NVSwitch) combines them; bdeg_finalize carry-normalises the four
-32-bit volume limbs into the exact 128-bit degree (include/bdeg.h).
+Each rank runs bdeg_degree_partial over its share of the work items into a
+16-slot int64 device buffer; one all-reduce(SUM) over NCCL (NVLink/NVSwitch)
+combines them; bdeg_finalize carry-normalises the four 32-bit volume limbs
+into the exact 128-bit degree (include/bdeg.h).
+
+Degeneracy ("almost all" liftings): the tie count travels
+in the same all-reduce.  Every rank sees the same summed slots, so every rank
+takes the same decision: a generated lifting is re-drawn on all ranks with the
+same attempt number (bdeg_relift, a deterministic derived seed) and the step
+is recomputed; a user lifting raises BDEG_E_DEGENERATE everywhere.
 """
 from __future__ import annotations
 
-from .bdeg import NSLOTS, Plan, Result
+from .bdeg import BDEG_E_DEGENERATE, BDEG_E_INVALID, NSLOTS, BdegError, Plan, Result
 
 MASK32 = (1 << 32) - 1
+SLOT_TIES = 7
 
 
 def pack_slots(volume: int, cells: int, singular: int, candidates: int, ties: int = 0,
@@ -30,8 +37,9 @@ def all_reduce_slots(slots, group=None):
 
 
 def enable_work_stealing(plan: Plan, device: int, group=None):
-    """All ranks draw work items from one queue in rank 0's GPU memory (CUDA
-    IPC + system-scope atomics over NVLink), instead of static shards."""
+    """All ranks draw the tail of the work items from one queue in rank 0's GPU
+    memory (CUDA IPC + system-scope atomics over NVLink) after their static
+    interleaved share (bdeg_steal_attach)."""
     import torch.distributed as dist
     from .bdeg import steal_create
     obj = [steal_create(device) if dist.get_rank(group) == 0 else None]
@@ -39,10 +47,45 @@ def enable_work_stealing(plan: Plan, device: int, group=None):
     plan.steal_attach(obj[0])     # rank 0 resolves its own handle locally
 
 
-def degree_distributed(plan: Plan, device, group=None) -> Result:
-    """This rank's shard on `device`, one all-reduce, exact finalize."""
+def combine_with_relift(plan: Plan, partial, reduce, max_relift: int = 32) -> Result:
+    """The collective degree protocol, independent of where the shard runs.
+
+    partial(plan) -> this rank's 16 slots (any object `reduce` accepts);
+    reduce(slots) -> the slots summed over all ranks, as a list of ints.
+    Repeats with bdeg_relift(attempt + 1) on every rank while the summed tie
+    count is non-zero (identical on all ranks, so all ranks agree)."""
+    attempt = plan.info().relifts
+    while True:
+        summed = reduce(partial(plan))
+        try:
+            return plan.finalize(summed)
+        except BdegError as e:
+            if e.status != BDEG_E_DEGENERATE or summed[SLOT_TIES] == 0:
+                raise
+            if attempt + 1 > max_relift:
+                raise BdegError(BDEG_E_DEGENERATE,
+                                f"no generic lifting within {max_relift} re-lifts") from e
+            try:
+                plan.relift(attempt + 1)
+            except BdegError as e2:       # a user lifting is never changed silently
+                if e2.status == BDEG_E_INVALID:
+                    raise e from None
+                raise
+            attempt += 1
+
+
+def degree_distributed(plan: Plan, device, group=None, max_relift: int = 32) -> Result:
+    """This rank's shard on `device`, one all-reduce per attempt, exact
+    finalize, collective re-lift on a degenerate generated lifting."""
     import torch
-    slots = torch.zeros(NSLOTS, dtype=torch.int64, device=device)
-    plan.degree_partial(slots.data_ptr())
-    all_reduce_slots(slots, group)
-    return plan.finalize(slots.cpu().tolist())
+
+    def partial(p):
+        slots = torch.zeros(NSLOTS, dtype=torch.int64, device=device)
+        p.degree_partial(slots.data_ptr())
+        return slots
+
+    def reduce(slots):
+        all_reduce_slots(slots, group)
+        return slots.cpu().tolist()
+
+    return combine_with_relift(plan, partial, reduce, max_relift)

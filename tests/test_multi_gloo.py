@@ -76,3 +76,64 @@ def test_sharded_combine_gloo(world):
         want = (full["volume"], full["cells"], full["singular"], full["candidates"])
         assert res[0][i] == res[1][i] == want
     assert res[0][1][0] == 14          # W_{2,2}: Table 3
+
+
+def _relift_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1501_02237_b200 as B
+    from paper_1501_02237_b200.multi import all_reduce_slots, combine_with_relift, pack_slots
+    from oracle.native import enumerate_range
+    # 2-bit generated liftings of W_{2,2}: degenerate at attempt 0
+    A, b = W.master_space_system(2, 2)
+    plan = B.Plan.from_system(A, b, seed=3, lift_bits=2, rank=rank, world=world)
+    attempts = []
+
+    def partial(p):
+        K, V, w = p.points()                 # the lifting in use on this attempt
+        attempts.append(p.info().seed_used)
+        acc = {"volume": 0, "cells": 0, "singular": 0, "candidates": 0, "ties": 0}
+        for it in p.shard_items(rank, world):
+            bb, e = p.item_range(it)
+            r = enumerate_range(K, V, w, bb, e)
+            for k in acc:
+                acc[k] += r[k]
+        return torch.tensor(pack_slots(acc["volume"], acc["cells"], acc["singular"],
+                                       acc["candidates"], acc["ties"]), dtype=torch.int64)
+
+    def reduce(slots):
+        all_reduce_slots(slots)
+        return slots.tolist()
+
+    res = combine_with_relift(plan, partial, reduce)
+    # a user lifting with ties is never re-lifted: every rank raises
+    K, V, w = plan.points()
+    flat = [7] * (len(A) + 1)
+    plan2 = B.Plan.from_system(A, b, flat, rank=rank, world=world)
+    try:
+        combine_with_relift(plan2, partial, reduce)
+        raised = None
+    except B.BdegError as e:
+        raised = e.status
+    q.put((rank, (res.degree, res.relifts, res.seed_used, tuple(attempts[:res.relifts + 1]), raised)))
+    dist.destroy_process_group()
+
+
+def test_collective_relift_gloo():
+    """Ties travel in the all-reduce; every rank re-lifts with the same attempt
+    (SURVEY §8.e degeneracy row) and the combined degree is exact."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_relift_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0][:4] == res[1][:4]
+    deg, relifts, seed, seeds, raised = res[0]
+    assert deg == 14 and relifts >= 1          # W_{2,2}: Table 3 (P:1646)
+    assert len(set(seeds)) == relifts + 1      # a fresh lifting per attempt
+    assert raised == 3 and res[1][4] == 3      # BDEG_E_DEGENERATE on every rank

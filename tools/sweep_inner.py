@@ -16,12 +16,14 @@ wls = sys.argv[1].split(",") if len(sys.argv) > 1 else ["c5", "w25", "w26"]
 Ss = [int(s) for s in sys.argv[2].split(",")] if len(sys.argv) > 2 else [2, 3, 4, 5, 6]
 torch.cuda.set_device(0)
 for wl in wls:
-    desc, K, V, w, extra = bench.workload(wl)
-    total = math.comb(len(V), K)
+    W = bench.Workload(wl)          # the library's own front end (bdeg_plan / bdeg_plan_points)
     for S in Ss:
-        if S > K - 1:
+        p = W.plan(inner_levels=S, flags=int(os.environ.get("SWEEP_FLAGS", "0"), 0))
+        info = p.info()
+        if S > info.K - 1:
+            p.close()
             continue
-        p = B.Plan.from_points(V, w, inner_levels=S, flags=int(os.environ.get("SWEEP_FLAGS", "0"), 0))
+        total = math.comb(info.N, info.K)
         r = p.degree()   # warm
         reps = 3 if total < 1e10 else 1
         t0 = time.perf_counter()
