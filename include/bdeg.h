@@ -45,7 +45,7 @@ typedef enum {
     BDEG_E_DEGENERATE = 3,    /* lifting not generic ("almost all"); user-given
                                  lifting, or max_relift generated liftings exhausted  */
     BDEG_E_IO = 4,            /* reserved (SPEC exit code 4)                           */
-    BDEG_E_TOO_LARGE = 5,     /* N > 64, K > 32, or an exact value exceeds 2^62        */
+    BDEG_E_TOO_LARGE = 5,     /* N > 128, K > 32, or an exact value exceeds 2^125      */
     BDEG_E_CUDA = 6,          /* CUDA runtime error / no sm_100 device                 */
     BDEG_E_COMM = 7           /* reserved for the multi-GPU combine                    */
 } bdeg_status;
@@ -100,7 +100,7 @@ typedef struct {
     uint64_t cells;          /* cells of the regular subdivision (lifting-dependent) */
     uint64_t singular;       /* K-subsets with det = 0 (lifting-independent)         */
     uint64_t ties;           /* would-be cells with a zero facet value (degenerate)  */
-    uint64_t overflow_reruns;/* blocks re-run in tier 2 after leaving their tier     */
+    uint64_t overflow_reruns;/* items re-run in tier 2 (int64) after leaving tier 0/1 */
     uint64_t updates;        /* fraction-free elimination updates executed          */
     uint64_t leaves;         /* (K-1)-prefixes tested (each = one warp-wide facet test) */
     uint64_t dead_leaves;    /* of which inside cell-dead subtrees (singular count only) */
@@ -110,6 +110,7 @@ typedef struct {
     uint64_t seed_used;      /* seed of the lifting that produced the result         */
     uint64_t total_candidates; /* C(N,K)                                             */
     double plan_ms, kernel_ms, total_ms;
+    uint64_t wide_reruns;    /* items re-run in the int128-value tier after leaving int64 */
 } bdeg_result;
 
 #define BDEG_NSLOTS 16       /* int64 partial-result slots combined by one all-reduce(SUM) */
@@ -157,19 +158,29 @@ bdeg_status bdeg_degree(bdeg_plan_t plan, bdeg_result *out);
  * C(c_i, i+1), c_0 < ... < c_{K-1}); no re-lift (ties are reported). */
 bdeg_status bdeg_degree_range(bdeg_plan_t plan, uint64_t begin, uint64_t end, bdeg_result *out);
 
-/* Work decomposition of the rank space (host only).  Item i is a tuple of
- * the largest subset indices; its candidates are the contiguous colex ranks
- * [*begin, *end).  Items partition [0, C(N,K)).  Sharding rule of
- * bdeg_degree_partial: rank r of world W takes the items i with
- * (num_items - 1 - i) mod W == r (largest items first). */
+/* Work decomposition of the rank space (host only).  Item i is
+ * the i-th position of the plan's work queue: a tuple of the largest subset
+ * indices whose candidates are the contiguous colex ranks [*begin, *end).
+ * Items partition [0, C(N,K)) and are listed largest-first: with world > 1,
+ * base-depth items larger than a quarter of a warp's share (C(N,K) / (world
+ * x SMs x resident warps)) are split one or more levels deeper.  Sharding
+ * rule of bdeg_degree_partial: rank r of world W takes the positions
+ * r, r + W, r + 2W, ... below n_static; the positions from n_static on are
+ * taken from the cross-GPU stealing counter (bdeg_steal_attach), `grab` per
+ * atomic, or, without it, by the same interleave (n_static = num_items). */
 uint64_t bdeg_num_items(bdeg_plan_t plan);
 bdeg_status bdeg_item_range(bdeg_plan_t plan, uint64_t item, uint64_t *begin, uint64_t *end);
+/* Queue shape: total positions, how many of them are split (finer-depth)
+ * items (they come first, sorted by size), the static prefix and the tail
+ * grab size.  Any pointer may be NULL. */
+bdeg_status bdeg_queue_info(bdeg_plan_t plan, uint64_t *n_items, uint64_t *n_split, uint64_t *n_static,
+                            uint64_t *grab);
 
 /* Result slots (int64, summed by the all-reduce): [0..3] the degree as four
  * 32-bit limbs (value = sum_i slot[i] << 32i), [4] cells, [5] singular,
- * [6] candidates, [7] ties, [8] blocks re-run in tier 2, [9] tier-2 overflow
- * (fatal), [10] re-run queue exhausted, [11] items, [12] updates, [13] leaves,
- * [14] dead leaves. */
+ * [6] candidates, [7] ties, [8] items re-run in tier 2, [9] values beyond
+ * the int128 tier (fatal), [10] unused (0), [11] items, [12] updates,
+ * [13] leaves, [14] dead leaves, [15] items re-run in the int128 tier. */
 
 /* This process's shard (options.rank of options.world) accumulated into the
  * caller's DEVICE buffer d_slots (BDEG_NSLOTS int64, zeroed here), async on
@@ -222,14 +233,27 @@ bdeg_status bdeg_steal_create(int32_t device, uint8_t *out_handle);
 bdeg_status bdeg_steal_attach(bdeg_plan_t plan, const uint8_t *handle);
 
 /* front end at scale (no plan needed).  Rank of A (n x m,
- * ROW-major int64) modulo a prime < 2^32 by GPU Gaussian row reduction (the
- * paper's GPU row reduction).  rank_p(A) <= rank_Q(A), equal
+ * ROW-major int64) modulo a prime < 2^31 by GPU Gaussian row reduction (the
+ * paper's GPU row reduction; one cooperative kernel, no host
+ * round trip per column).  rank_p(A) <= rank_Q(A), equal
  * unless p divides every maximal non-zero minor.  bdeg_dimension_modp returns
  * n - max(rank_p) over the primes 2^31-1 and 2^31-19 (probabilistic, pinned by
  * the paper's Tables 1-2; the exact dimension comes from bdeg_plan's SNF). */
 bdeg_status bdeg_rank_modp(int32_t n, int32_t m, const int64_t *A, uint32_t prime, int32_t device, void *stream,
                            int64_t *rank);
 bdeg_status bdeg_dimension_modp(int32_t n, int32_t m, const int64_t *A, int32_t device, int32_t *dim);
+
+/* EXACT rank and component count at scale (no plan needed).
+ * One cooperative GPU kernel eliminates A (n x m, ROW-major int64) over Z
+ * with unit pivots only (+-1 entries: each is an invariant factor 1 of the
+ * Smith form); the rows never used x the columns left without a
+ * unit pivot form a residual block whose Smith form the host finishes
+ * exactly (Euclidean, checked int128).  Returns rank A (dimension n - rank,
+ * Prop. 1), |prod d_j| (the number of components) as two 64-bit
+ * halves, and how many unit pivots the GPU found.  BDEG_E_TOO_LARGE when an
+ * entry would pass 2^61 or the residual exceeds 4e6 entries. */
+bdeg_status bdeg_smith_gpu(int32_t n, int32_t m, const int64_t *A, int32_t device, void *stream, int64_t *rank,
+                           uint64_t *comp_lo, uint64_t *comp_hi, int64_t *unit_pivots);
 
 /* Carry-normalise summed slots (HOST memory) into *out. */
 bdeg_status bdeg_finalize(bdeg_plan_t plan, const int64_t *h_slots, bdeg_result *out);

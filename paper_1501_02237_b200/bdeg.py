@@ -34,7 +34,7 @@ FLAG_FORCE_TIER1 = 0x8
 FLAG_NO_RELIFT = 0x10
 FLAG_FORCE_TIER2 = 0x20
 FLAG_DEGREE_ONLY = 0x40
-TIER_DTYPE = {0: "int32", 1: "int32/int64", 2: "int64/int128"}
+TIER_DTYPE = {0: "int32", 1: "int32/int64", 2: "int64/int128", 4: "int128/int256"}
 
 NSLOTS = 16
 
@@ -76,7 +76,7 @@ class _Result(ctypes.Structure):
                 ("seed_used", ctypes.c_uint64),
                 ("total_candidates", ctypes.c_uint64),
                 ("plan_ms", ctypes.c_double), ("kernel_ms", ctypes.c_double),
-                ("total_ms", ctypes.c_double)]
+                ("total_ms", ctypes.c_double), ("wide_reruns", ctypes.c_uint64)]
 
 
 EXPORTS = ["bdeg_default_options", "bdeg_plan", "bdeg_plan_points", "bdeg_plan_info",
@@ -85,7 +85,7 @@ EXPORTS = ["bdeg_default_options", "bdeg_plan", "bdeg_plan_points", "bdeg_plan_i
            "bdeg_status_str", "bdeg_destroy", "bdeg_launch_count", "bdeg_num_items",
            "bdeg_item_range", "bdeg_cells", "bdeg_degree_walk", "bdeg_cell_normal",
            "bdeg_steal_create", "bdeg_steal_attach", "bdeg_rank_modp", "bdeg_dimension_modp",
-           "bdeg_plan_points_get"]
+           "bdeg_plan_points_get", "bdeg_queue_info", "bdeg_smith_gpu"]
 
 
 def _load():
@@ -120,6 +120,9 @@ def _load():
     lib.bdeg_num_items.restype = ctypes.c_uint64
     lib.bdeg_item_range.argtypes = [plan_t, ctypes.c_uint64, P(ctypes.c_uint64), P(ctypes.c_uint64)]
     lib.bdeg_item_range.restype = ctypes.c_int
+    lib.bdeg_queue_info.argtypes = [plan_t, P(ctypes.c_uint64), P(ctypes.c_uint64), P(ctypes.c_uint64),
+                                    P(ctypes.c_uint64)]
+    lib.bdeg_queue_info.restype = ctypes.c_int
     lib.bdeg_cells.argtypes = [plan_t, ctypes.c_uint64, ctypes.c_uint64, P(ctypes.c_uint64),
                                ctypes.c_uint64, P(ctypes.c_uint64)]
     lib.bdeg_cells.restype = ctypes.c_int
@@ -138,6 +141,10 @@ def _load():
     lib.bdeg_dimension_modp.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int64), ctypes.c_int32,
                                         P(ctypes.c_int32)]
     lib.bdeg_dimension_modp.restype = ctypes.c_int
+    lib.bdeg_smith_gpu.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int64), ctypes.c_int32,
+                                   ctypes.c_void_p, P(ctypes.c_int64), P(ctypes.c_uint64), P(ctypes.c_uint64),
+                                   P(ctypes.c_int64)]
+    lib.bdeg_smith_gpu.restype = ctypes.c_int
     lib.bdeg_launch_count.argtypes = []
     lib.bdeg_launch_count.restype = ctypes.c_uint64
     for name in ["bdeg_plan", "bdeg_plan_points", "bdeg_plan_info", "bdeg_plan_points_get", "bdeg_set_workspace",
@@ -165,6 +172,18 @@ def dimension_modp(A, device=None) -> int:
     d = ctypes.c_int32()
     _check(lib.bdeg_dimension_modp(n, m, buf, _current_device() if device is None else device, ctypes.byref(d)))
     return d.value
+
+
+def smith_gpu(A, device=None):
+    """Exact (rank, |prod d_j|, unit pivots) of A by GPU unit-pivot elimination
+    plus the host Smith form of the residual (bdeg_smith_gpu)."""
+    n = len(A)
+    m = len(A[0]) if n else 0
+    buf = _i64([A[i][j] for i in range(n) for j in range(m)])
+    r, lo, hi, piv = ctypes.c_int64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_int64()
+    _check(lib.bdeg_smith_gpu(n, m, buf, _current_device() if device is None else device, None,
+                              ctypes.byref(r), ctypes.byref(lo), ctypes.byref(hi), ctypes.byref(piv)))
+    return r.value, (hi.value << 64) | lo.value, piv.value
 
 
 def launch_count() -> int:
@@ -199,6 +218,7 @@ class Result:
     plan_ms: float
     kernel_ms: float
     total_ms: float
+    wide_reruns: int = 0
     extra: dict = field(default_factory=dict)
 
 
@@ -214,7 +234,7 @@ def _result(r: _Result) -> Result:
                   consistent=bool(r.consistent), singular_complete=bool(r.singular_complete),
                   seed_used=r.seed_used,
                   total_candidates=r.total_candidates, plan_ms=r.plan_ms,
-                  kernel_ms=r.kernel_ms, total_ms=r.total_ms)
+                  kernel_ms=r.kernel_ms, total_ms=r.total_ms, wide_reruns=r.wide_reruns)
 
 
 def _current_device():
@@ -342,10 +362,16 @@ class Plan:
         _check(lib.bdeg_item_range(self._h, item, ctypes.byref(b), ctypes.byref(e)), self._h)
         return b.value, e.value
 
+    def queue_info(self):
+        """dict(n_items, n_split, n_static, grab) of the work queue (bdeg_queue_info)."""
+        v = [ctypes.c_uint64() for _ in range(4)]
+        _check(lib.bdeg_queue_info(self._h, *[ctypes.byref(x) for x in v]), self._h)
+        return dict(zip(("n_items", "n_split", "n_static", "grab"), (x.value for x in v)))
+
     def shard_items(self, rank: int, world: int):
-        """Items of `rank` under bdeg_degree_partial's sharding rule."""
-        n = self.num_items()
-        return [n - 1 - (rank + i * world) for i in range((n - rank + world - 1) // world) if n - 1 - (rank + i * world) >= 0]
+        """Queue positions of `rank` under bdeg_degree_partial's static rule
+        (no stealing counter attached): rank, rank + world, ..."""
+        return list(range(rank, self.num_items(), world))
 
     def steal_attach(self, handle: bytes):
         """Take work items from the shared cross-GPU queue (bdeg_steal_attach)."""

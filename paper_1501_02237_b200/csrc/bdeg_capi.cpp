@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -38,7 +39,10 @@ struct bdeg_plan_s {
     unsigned long long *steal = nullptr;   // cross-GPU item counters (2, by step parity), IPC-mapped
     int steal_parity = 0;
     uint64_t basis_lo = 0, basis_hi = 0;   // basis-seeded start cell (N > 64, generated lifting)
-    uint64_t nblocks = 0, total = 0;
+    uint64_t nblocks = 0, total = 0;      // base-depth items (colex range mode), C(N,K)
+    std::vector<uint64_t> split;          // work queue (build_queue): split items, then groups
+    std::vector<uint64_t> grp_u, grp_cum;
+    uint64_t nitems = 0, nstatic_steal = 0, grab = 1;
     uint64_t seed_used = 0;
     int relifts = 0;
     double plan_ms = 0;
@@ -48,9 +52,10 @@ struct bdeg_plan_s {
     char *ws = nullptr;
     size_t ws_bytes = 0;
     unsigned long long *d_slots = nullptr, *d_ctr = nullptr, *d_ovfq = nullptr;
+    uint64_t *d_split = nullptr, *d_gu = nullptr, *d_gc = nullptr;
     int64_t *d_L = nullptr;
     uint64_t *d_B = nullptr;
-    uint64_t ovf_cap = 1 << 16;
+    uint64_t ovf_words = 1;               // re-run bitmap: one bit per work-queue position
     int grid = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<uint64_t> binom;
@@ -88,8 +93,10 @@ void fill_binom(std::vector<uint64_t> &B) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // workspace layout
+constexpr int kMaxGroups = 66;
+constexpr uint64_t kMaxOvfWords = 1ull << 21;   // base-depth item groups (one per smallest top index u)
 struct Layout {
-    size_t slots, ctr, L, B, q, total;
+    size_t slots, ctr, L, B, q, split, gu, gc, total;
 };
 Layout layout(const bdeg_plan_s *p) {
     Layout l;
@@ -98,7 +105,10 @@ Layout layout(const bdeg_plan_s *p) {
     l.ctr = off;   off = align256(off + 8 * 8);
     l.L = off;     off = align256(off + (((size_t)(p->K + 1) * p->N * 8 + 15) & ~(size_t)15));
     l.B = off;     off = align256(off + (size_t)kBinomRows * kBinomCols * 8);
-    l.q = off;     off = align256(off + p->ovf_cap * 8);
+    l.q = off;     off = align256(off + 2 * p->ovf_words * 8);   // bitmaps A (narrow -> int64), B (-> int128)
+    l.split = off; off = align256(off + std::max<size_t>(1, p->split.size()) * 8);
+    l.gu = off;    off = align256(off + kMaxGroups * 8);
+    l.gc = off;    off = align256(off + kMaxGroups * 8);
     l.total = off;
     return l;
 }
@@ -232,6 +242,172 @@ void raw_tier_bounds(bdeg_plan_s *p) {
     if (p->tier == 1 && (mv >= ((int64_t)1 << p->bits_v) || mw >= ((int64_t)1 << p->bits_l))) p->tier = 2;
 }
 
+// Per-device properties (queried once per process) and a small pool of
+// device workspaces, so that planning a new problem does not pay
+// cudaGetDeviceProperties / cudaMalloc / cudaFree every time.
+struct DevInfo { bool ok = false; int sms = 0, major = 0; };
+std::mutex g_mu;
+constexpr int kMaxDevices = 64;
+DevInfo g_dev[kMaxDevices];
+std::vector<std::pair<size_t, void *>> g_pool[kMaxDevices];
+std::map<std::string, void *> g_steal_local;   // IPC handles exported by this process
+
+DevInfo g_dev_none;
+
+const DevInfo &dev_info(int d) {
+    if (d < 0 || d >= kMaxDevices) return g_dev_none;   // ok = false
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_dev[d].ok) {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, d) == cudaSuccess) {
+            g_dev[d].sms = prop.multiProcessorCount;
+            g_dev[d].major = prop.major;
+            g_dev[d].ok = true;
+        }
+    }
+    return g_dev[d];
+}
+
+// ------------------------------------------------------------ work queue
+// SURVEY §8.e.  Items are tuples of the largest subset indices (c_{K-d} <
+// ... < c_{K-1}); an item of depth d whose smallest index is u holds the
+// C(u, K-d) candidates below it (a contiguous colex rank interval).  The
+// queue lists the items largest-first: (1) items split to a finer depth (only
+// for world > 1: base-depth items larger than a quarter of a warp's share are
+// cut one level deeper, recursively), sorted by size; (2) the other base-depth
+// items grouped by u, u descending (group g = every (D-1)-subset of
+// {u+1..N-1} above u, in colex order).  Positions [0, nstatic) are
+// interleaved over the ranks; with cross-GPU stealing the rest is taken from
+// one global counter, `grab` positions per atomic.
+inline uint64_t colex_id(const std::vector<uint64_t> &B, const int *c, int d, int shift) {
+    uint64_t id = 0;
+    for (int t = 0; t < d; ++t) id += C(B, c[t] - shift, t + 1);
+    return id;
+}
+
+int warps_per_sm_estimate(const bdeg_plan_s *p) {
+    const int ctas_lb = p->S >= 5 ? 3 : 4;               // __launch_bounds__ of k_enumerate
+    const size_t smem = enumerate_smem_bytes(p->K, p->N, kernel_warps_per_cta());
+    const int ctas_sm = (int)std::max<size_t>(1, (228 * 1024) / (smem + 1024));
+    return std::min(ctas_lb, ctas_sm) * kernel_warps_per_cta();
+}
+
+void build_queue(bdeg_plan_s *p) {
+    const int K = p->K, N = p->N, D = p->D;
+    const auto &B = p->binom;
+    p->split.clear();
+    p->grp_u.clear();
+    p->grp_cum.clear();
+    const int world = std::max(1, p->opt.world);
+    const DevInfo &di = dev_info(p->opt.device);
+    const double sms = di.ok ? di.sms : 148.0;
+    const double warps = sms * warps_per_sm_estimate(p);
+    double frac = 0.25;                                   // largest item <= frac x a warp's share
+    if (const char *e = std::getenv("BDEG_SPLIT_SHARE")) frac = std::atof(e);
+    const bool do_split = (world > 1 || std::getenv("BDEG_SPLIT_1GPU")) && D > 0 && frac > 0;
+    const double cap = std::max(1.0, (double)p->total / (world * warps) * frac);
+    std::vector<std::pair<uint64_t, uint64_t>> sp;        // (size, depth << 58 | id)
+    if (D == 0) {
+        p->grp_u.push_back(N);
+        p->grp_cum = {0, 1};
+    } else {
+        uint64_t cum = 0;
+        for (int u = N - D; u >= K - D; --u) {
+            const uint64_t cnt = C(B, N - 1 - u, D - 1), sz = C(B, u, K - D);
+            if (cnt == 0) continue;
+            if (!do_split || (double)sz <= cap || D >= K - 1) {
+                p->grp_u.push_back(u);
+                p->grp_cum.push_back(cum);
+                cum += cnt;
+                continue;
+            }
+            // every item of the group: u, then a (D-1)-subset of {u+1..N-1} (colex successor)
+            std::vector<int> top(D);
+            top[0] = u;
+            for (int t = 1; t < D; ++t) top[t] = u + t;
+            for (;;) {
+                // recursive split of the tuple (smallest first) down to size <= cap
+                std::vector<std::pair<std::vector<int>, int>> st{{top, D}};
+                while (!st.empty()) {
+                    auto [tp, d] = st.back();
+                    st.pop_back();
+                    const uint64_t size = C(B, tp[0], K - d);
+                    if ((double)size <= cap || d >= K - 1) {
+                        sp.push_back({size, ((uint64_t)d << 58) | colex_id(B, tp.data(), d, K - d)});
+                        continue;
+                    }
+                    for (int u2 = K - d - 1; u2 < tp[0]; ++u2) {
+                        std::vector<int> ch(d + 1);
+                        ch[0] = u2;
+                        std::copy(tp.begin(), tp.end(), ch.begin() + 1);
+                        st.push_back({ch, d + 1});
+                    }
+                }
+                int t = 1;                                // next (D-1)-subset of {u+1..N-1}
+                while (t < D && (t + 1 < D ? top[t] + 1 >= top[t + 1] : top[t] + 1 >= N)) ++t;
+                if (t >= D) break;
+                ++top[t];
+                for (int q = 1; q < t; ++q) top[q] = u + q;
+            }
+        }
+        p->grp_cum.push_back(cum);
+    }
+    std::stable_sort(sp.begin(), sp.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
+    p->split.resize(sp.size());
+    for (size_t i = 0; i < sp.size(); ++i) p->split[i] = sp[i].second;
+    p->nitems = p->split.size() + p->grp_cum.back();
+    // static share: the positions holding the first ~80% of the candidates
+    // (balanced by the interleave); the rest is the stealing tail
+    uint64_t acc = 0, pos = 0;
+    const double want = 0.8 * (double)p->total;
+    for (size_t i = 0; i < sp.size() && acc < want; ++i, ++pos) acc += sp[i].first;
+    for (size_t g = 0; g + 1 < p->grp_cum.size() && acc < want; ++g) {
+        const uint64_t cnt = p->grp_cum[g + 1] - p->grp_cum[g];
+        const uint64_t sz = D == 0 ? p->total : C(B, p->grp_u[g], K - D);
+        const uint64_t need = sz ? (uint64_t)std::ceil((want - (double)acc) / (double)sz) : cnt;
+        const uint64_t take = std::min(cnt, need);
+        acc += take * sz;
+        pos += take;
+    }
+    p->nstatic_steal = world > 1 ? std::min(pos, p->nitems) : p->nitems;
+    const uint64_t tail = p->nitems - p->nstatic_steal;
+    p->grab = std::max<uint64_t>(1, tail / (uint64_t)std::max(1.0, world * warps * 4));
+}
+
+// queue position -> (depth, tuple of the largest indices, smallest first)
+void decode_position(const bdeg_plan_s *p, uint64_t pos, int &d, std::vector<int> &top) {
+    const auto &B = p->binom;
+    const int K = p->K;
+    top.clear();
+    if (pos < p->split.size()) {
+        d = (int)(p->split[pos] >> 58);
+        uint64_t r = p->split[pos] & ((1ull << 58) - 1);
+        top.assign(d, 0);
+        for (int t = d - 1; t >= 0; --t) {
+            int x = t;
+            while (C(B, x + 1, t + 1) <= r) ++x;
+            r -= C(B, x, t + 1);
+            top[t] = x + K - d;
+        }
+        return;
+    }
+    d = p->D;
+    if (d == 0) return;
+    const uint64_t q = pos - p->split.size();
+    size_t g = 0;
+    while (g + 2 < p->grp_cum.size() && p->grp_cum[g + 1] <= q) ++g;
+    const int u = p->grp_u[g];
+    uint64_t r = q - p->grp_cum[g];
+    top.assign(d, 0);
+    top[0] = u;
+    for (int t = d - 2; t >= 0; --t) {
+        int x = t;
+        while (C(B, x + 1, t + 1) <= r) ++x;
+        r -= C(B, x, t + 1);
+        top[t + 1] = x + u + 1;
+    }
+}
+
 void choose_tier_and_blocks(bdeg_plan_s *p) {
     p->total = C(p->binom, p->N, p->K);
     int bv = 0, bl = 0;
@@ -283,6 +459,7 @@ void choose_tier_and_blocks(bdeg_plan_s *p) {
     while (D < p->K - 1 && (double)C(p->binom, p->N - D, p->K - D) > limit) ++D;
     p->D = D;
     p->nblocks = C(p->binom, p->N - p->K + p->D, p->D);
+    build_queue(p);
 }
 
 // Greedy basis of the point vectors (first K linearly independent points,
@@ -341,11 +518,47 @@ bdeg_status finish_plan(bdeg_plan_s *p) {
                                               std::to_string(p->N) + ", K=" + std::to_string(p->K) + ")");
     p->big = p->N > kMaxN;
     for (int64_t v : p->V)
-        if (v > ((int64_t)1 << 40) || v < -((int64_t)1 << 40))
-            return fail(p, BDEG_E_TOO_LARGE, "point coordinate beyond 2^40");
+        if (v >= ((int64_t)1 << 62) || v <= -((int64_t)1 << 62))
+            return fail(p, BDEG_E_TOO_LARGE, "point coordinate beyond 2^62");
     for (int64_t v : p->w)
-        if (v > ((int64_t)1 << 52) || v < -((int64_t)1 << 52))
-            return fail(p, BDEG_E_TOO_LARGE, "lifting value beyond 2^52");
+        if (v >= ((int64_t)1 << 62) || v <= -((int64_t)1 << 62))
+            return fail(p, BDEG_E_TOO_LARGE, "lifting value beyond 2^62");
+    // Every value the elimination stores is a minor of the lifted (K+1) x N
+    // matrix (Sylvester's identity).  Hadamard: a minor of V rows only is at
+    // most H_V = the product of the K largest column norms of V; expanding a
+    // minor with the lift row along that row, it is at most (K+1) max|w| H_V.
+    // Below 2^125 the int128-value tier (the end of the overflow chain) can
+    // never overflow.
+    {
+        std::vector<double> lg(p->N, 0.0);
+        double wmax = 1;
+        for (int l = 0; l < p->N; ++l) {
+            long double n2 = 0;
+            for (int i = 0; i < p->K; ++i) n2 += (long double)p->V[(size_t)l * p->K + i] * p->V[(size_t)l * p->K + i];
+            lg[l] = n2 > 1 ? 0.5 * std::log2((double)n2) : 0.0;
+            wmax = std::max(wmax, std::fabs((double)p->w[l]));
+        }
+        std::sort(lg.begin(), lg.end(), [](double a, double b) { return a > b; });
+        double hv = 0;
+        for (int i = 0; i < std::min(p->K, p->N); ++i) hv += lg[i];
+        // the same by rows (tighter when a row is small, e.g. the row of ones
+        // of an affine configuration): each row restricted to its K largest
+        // entries, factors below 1 counted as 1 (minors of fewer rows)
+        double hr = 0;
+        for (int i = 0; i < p->K; ++i) {
+            std::vector<long double> sq(p->N);
+            for (int l = 0; l < p->N; ++l) sq[l] = (long double)p->V[(size_t)l * p->K + i] * p->V[(size_t)l * p->K + i];
+            std::sort(sq.begin(), sq.end(), [](long double a, long double b) { return a > b; });
+            long double n2 = 0;
+            for (int l = 0; l < std::min(p->K, p->N); ++l) n2 += sq[l];
+            hr += n2 > 1 ? 0.5 * std::log2((double)n2) : 0.0;
+        }
+        hv = std::min(hv, hr);
+        const double bound = std::max(hv, std::log2((double)(p->K + 1)) + std::log2(wmax) + hv);
+        if (bound >= 124.9)
+            return fail(p, BDEG_E_TOO_LARGE, "Hadamard bound of the lifted minors is 2^" + std::to_string((int)bound) +
+                                                 " >= 2^125 (beyond the int128 tier)");
+    }
     if (p->big) {
         // walk only: no rank space (C(N,K) may exceed 2^64), no enumeration items
         int bv = 0, bl = 0;
@@ -364,8 +577,11 @@ bdeg_status finish_plan(bdeg_plan_s *p) {
     } else {
         choose_tier_and_blocks(p);
     }
-    // one re-run queue entry per work item: the queue cannot be exhausted
-    p->ovf_cap = std::max<uint64_t>(1, p->nblocks);
+    // the re-run bitmaps have one bit per work item (either mode), up to 2^27
+    // items (16 MB each); positions beyond that are counted in SLOT_QFULL and
+    // the synchronous entry points redo the whole space in tier 2
+    p->ovf_words = std::min<uint64_t>((std::max<uint64_t>(std::max(p->nblocks, p->nitems), 1) + 63) / 64,
+                                      kMaxOvfWords);
     p->l_dirty = true;
     return BDEG_OK;
 }
@@ -374,32 +590,6 @@ bdeg_status finish_plan(bdeg_plan_s *p) {
 void rebuild_points(bdeg_plan_s *p) {
     build_points(p->fe, p->lift.data(), !(p->opt.flags & BDEG_FLAG_NO_HOMOG_SHORTCUT), p->K, p->N, p->V,
                  p->w, p->point_of_var, p->origin_index);
-}
-
-// Per-device properties (queried once per process) and a small pool of
-// device workspaces, so that planning a new problem does not pay
-// cudaGetDeviceProperties / cudaMalloc / cudaFree every time.
-struct DevInfo { bool ok = false; int sms = 0, major = 0; };
-std::mutex g_mu;
-constexpr int kMaxDevices = 64;
-DevInfo g_dev[kMaxDevices];
-std::vector<std::pair<size_t, void *>> g_pool[kMaxDevices];
-std::map<std::string, void *> g_steal_local;   // IPC handles exported by this process
-
-DevInfo g_dev_none;
-
-const DevInfo &dev_info(int d) {
-    if (d < 0 || d >= kMaxDevices) return g_dev_none;   // ok = false
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (!g_dev[d].ok) {
-        cudaDeviceProp prop;
-        if (cudaGetDeviceProperties(&prop, d) == cudaSuccess) {
-            g_dev[d].sms = prop.multiProcessorCount;
-            g_dev[d].major = prop.major;
-            g_dev[d].ok = true;
-        }
-    }
-    return g_dev[d];
 }
 
 void *pool_get(int d, size_t bytes, size_t *got) {
@@ -462,9 +652,25 @@ bdeg_status ensure_device(bdeg_plan_s *p) {
         p->d_L = reinterpret_cast<int64_t *>(p->ws + L.L);
         p->d_B = reinterpret_cast<uint64_t *>(p->ws + L.B);
         p->d_ovfq = reinterpret_cast<unsigned long long *>(p->ws + L.q);
+        if ((e = cudaMemsetAsync(p->d_ovfq, 0, 2 * p->ovf_words * 8, (cudaStream_t)p->opt.stream)) != cudaSuccess)
+            return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));      // the replay keeps it clean after this
+        p->d_split = reinterpret_cast<uint64_t *>(p->ws + L.split);
+        p->d_gu = reinterpret_cast<uint64_t *>(p->ws + L.gu);
+        p->d_gc = reinterpret_cast<uint64_t *>(p->ws + L.gc);
         cudaStream_t st = (cudaStream_t)p->opt.stream;
         if ((e = cudaMemcpyAsync(p->d_B, p->binom.data(), p->binom.size() * 8, cudaMemcpyHostToDevice, st)) !=
             cudaSuccess)
+            return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
+        // the work queue (plan-constant): split items and the group tables
+        if (!p->split.empty() &&
+            (e = cudaMemcpyAsync(p->d_split, p->split.data(), p->split.size() * 8, cudaMemcpyHostToDevice, st)) !=
+                cudaSuccess)
+            return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
+        if (!p->grp_u.empty() &&
+            ((e = cudaMemcpyAsync(p->d_gu, p->grp_u.data(), p->grp_u.size() * 8, cudaMemcpyHostToDevice, st)) !=
+                 cudaSuccess ||
+             (e = cudaMemcpyAsync(p->d_gc, p->grp_cum.data(), p->grp_cum.size() * 8, cudaMemcpyHostToDevice, st)) !=
+                 cudaSuccess))
             return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
         if ((e = cudaEventCreate(&p->ev0)) != cudaSuccess || (e = cudaEventCreate(&p->ev1)) != cudaSuccess)
             return fail(p, BDEG_E_CUDA, std::string("cudaEventCreate: ") + cudaGetErrorString(e));
@@ -512,14 +718,27 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     a.P.K = p->K; a.P.N = p->N; a.P.S = p->S; a.P.T = p->T; a.P.D = p->D;
     a.rank_begin = b;
     a.rank_end = e;
-    a.blk_first = block_of(p, b);
-    a.blk_last = block_of(p, e - 1);
-    a.blk_offset = (uint64_t)rank;
-    a.blk_stride = (uint64_t)std::max(world, 1);
+    a.rank = rank;
+    a.world = std::max(world, 1);
+    if (b == 0 && e >= p->total) {        // the whole space: the largest-first work queue
+        a.mode = 1;
+        a.split = p->d_split;
+        a.n_split = p->split.size();
+        a.grp_u = p->d_gu;
+        a.grp_cum = p->d_gc;
+        a.n_grp = (int)p->grp_u.size();
+        a.n_items = p->nitems;
+    } else {                              // a rank range: contiguous base-depth items
+        a.mode = 0;
+        a.blk_first = block_of(p, b);
+        a.blk_last = block_of(p, e - 1);
+        a.n_items = a.blk_last - a.blk_first + 1;
+    }
+    a.n_static = a.n_items;
+    a.grab = 1;
     a.slots = slots;
-    a.ovf_queue = p->d_ovfq;
-    a.ovf_count = p->d_ctr + 2;
-    a.ovf_cap = p->ovf_cap;
+    a.ovf_words = std::min<uint64_t>((a.n_items + 63) / 64, p->ovf_words);
+    unsigned long long *bitsA = p->d_ovfq, *bitsB = p->d_ovfq + p->ovf_words;
     a.grid = p->grid;
     a.stream = st;
     a.tier = force_tier >= 0 ? force_tier : p->tier;
@@ -536,25 +755,40 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     a.bits_l = p->bits_l;
     a.replay = 0;
     a.counter = p->d_ctr + 0;
-    if (p->steal && world > 1) {        // one global largest-first queue over all GPUs
-        a.counter = p->steal + p->steal_parity;
+    if (p->steal && world > 1 && a.mode == 1) {
+        // static interleaved share of the first ~80% of the candidates, then
+        // one global tail queue over all GPUs (system-scope atomics, NVLink)
+        a.n_static = p->nstatic_steal;
+        a.grab = p->grab;
+        a.gcounter = p->steal + p->steal_parity;
         a.system_counter = 1;
-        a.blk_offset = 0;
-        a.blk_stride = 1;
         if (rank == 0) a.reset_next = p->steal + (p->steal_parity ^ 1);
         p->steal_parity ^= 1;
     }
+    // overflow chain: an item that leaves its tier is marked
+    // and redone by the next one — narrow (tiers 0/1/3) -> tier 2 (int64
+    // values, checked int128 products) -> tier 4 (int128 values, 256-bit)
+    a.mark_bits = a.tier == 2 ? bitsB : bitsA;
     int rc = launch_enumerate(a);
     if (rc) return fail(p, BDEG_E_CUDA, std::string("k_enumerate launch: ") + cudaGetErrorString((cudaError_t)rc));
-    if (a.tier != 2) {   // re-run the blocks that left their tier, in int64/int128
+    a.replay = 1;
+    a.gcounter = nullptr;
+    a.system_counter = 0;
+    a.reset_next = nullptr;
+    a.stop_on_cell = 0;
+    if (a.tier != 2) {
         a.tier = 2;
-        a.replay = 1;
         a.counter = p->d_ctr + 1;
-        a.system_counter = 0;
-        a.reset_next = nullptr;
+        a.replay_bits = bitsA;
+        a.mark_bits = bitsB;
         rc = launch_enumerate(a);
         if (rc) return fail(p, BDEG_E_CUDA, std::string("k_enumerate replay: ") + cudaGetErrorString((cudaError_t)rc));
     }
+    a.counter = p->d_ctr + 3;
+    a.replay_bits = bitsB;
+    a.mark_bits = nullptr;
+    rc = launch_enumerate_wide(a);
+    if (rc) return fail(p, BDEG_E_CUDA, std::string("k_enumerate_wide: ") + cudaGetErrorString((cudaError_t)rc));
     return BDEG_OK;
 }
 
@@ -580,7 +814,7 @@ void fill_front(const bdeg_plan_s *p, bdeg_result *r) {
 
 bdeg_status slots_to_result(bdeg_plan_s *p, const int64_t *h, bdeg_result *r) {
     if (h[SLOT_FATAL] > 0)
-        return fail(p, BDEG_E_TOO_LARGE, "an exact elimination value exceeded the int64 tier (|v| >= 2^62)");
+        return fail(p, BDEG_E_TOO_LARGE, "an exact elimination value exceeded the int128 tier (|v| >= 2^125)");
     u128 vol = 0;
     for (int i = 3; i >= 0; --i) vol = (vol << 32) + (u128)(uint64_t)h[SLOT_VOL0 + i];
     r->deg_lo = (uint64_t)vol;
@@ -590,6 +824,7 @@ bdeg_status slots_to_result(bdeg_plan_s *p, const int64_t *h, bdeg_result *r) {
     r->candidates = (uint64_t)h[SLOT_CAND];
     r->ties = (uint64_t)h[SLOT_TIES];
     r->overflow_reruns = (uint64_t)h[SLOT_OVF_BLOCKS];
+    r->wide_reruns = (uint64_t)h[SLOT_WIDE];
     r->updates = (uint64_t)h[SLOT_UPDATES];
     r->leaves = (uint64_t)h[SLOT_LEAVES];
     r->dead_leaves = (uint64_t)h[SLOT_DEAD];
@@ -597,7 +832,7 @@ bdeg_status slots_to_result(bdeg_plan_s *p, const int64_t *h, bdeg_result *r) {
 }
 
 // one synchronous pass over [b, e) on this GPU; re-runs everything in the
-// int64 tier if the overflow queue was exhausted.
+// int64 tier if an overflowing item lay beyond the re-run bitmap.
 bdeg_status run_sync(bdeg_plan_s *p, uint64_t b, uint64_t e, int64_t *h, double *kms) {
     cudaStream_t st = (cudaStream_t)p->opt.stream;
     bdeg_status s = ensure_device(p);
@@ -615,7 +850,7 @@ bdeg_status run_sync(bdeg_plan_s *p, uint64_t b, uint64_t e, int64_t *h, double 
         *kms += ms;
         if (h[SLOT_QFULL] == 0) return BDEG_OK;
     }
-    return BDEG_OK;
+    return fail(p, BDEG_E_TOO_LARGE, "values beyond int64 in more work items than the re-run bitmap holds");
 }
 
 // Device buffers of one walk (freed on scope exit).
@@ -648,9 +883,9 @@ bdeg_status cells_range(bdeg_plan_s *p, uint64_t b, uint64_t e, uint64_t *h_out,
     cudaMemcpyAsync(h, p->d_slots, kNSlots * 8, cudaMemcpyDeviceToHost, st);
     cudaError_t ce = cudaStreamSynchronize(st);
     if (ce != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
-    // tier 2 only (no replay): an item whose values left int64 dropped its cells
+    // tier 2, then tier 4 for the items whose values left int64
     if (h[SLOT_FATAL] > 0)
-        return fail(p, BDEG_E_TOO_LARGE, "cell emission: an exact elimination value exceeded the int64 tier");
+        return fail(p, BDEG_E_TOO_LARGE, "cell emission: an exact elimination value exceeded the int128 tier");
     // a would-be cell on a tie: the lifting is not generic, the list is not a subdivision
     if (h[SLOT_TIES] > 0)
         return fail(p, BDEG_E_DEGENERATE, "degenerate lifting: a would-be cell has a zero facet value");
@@ -1178,9 +1413,10 @@ bdeg_status bdeg_finalize(bdeg_plan_t p, const int64_t *h_slots, bdeg_result *ou
         *out = r;
         return BDEG_OK;
     }
-    // the re-run queue holds one entry per work item, so it cannot be exhausted
+    // more than 2^27 work items and an overflow beyond the re-run bitmap
     if (h_slots[SLOT_QFULL] > 0)
-        return fail(p, BDEG_E_TOO_LARGE, "overflow re-run queue exhausted (internal error)");
+        return fail(p, BDEG_E_TOO_LARGE, "overflow re-run bitmap exhausted (> 2^27 work items); rerun with "
+                                         "BDEG_FLAG_FORCE_TIER2");
     bdeg_status s = slots_to_result(p, h_slots, &r);
     if (s) return s;
     // a would-be cell with a zero facet value on any rank: the lifting is not
@@ -1194,24 +1430,30 @@ bdeg_status bdeg_finalize(bdeg_plan_t p, const int64_t *h_slots, bdeg_result *ou
     return BDEG_OK;
 }
 
-uint64_t bdeg_num_items(bdeg_plan_t p) { return (p && p->K > 0) ? p->nblocks : 0; }
+uint64_t bdeg_num_items(bdeg_plan_t p) { return (p && p->K > 0) ? p->nitems : 0; }
 
 bdeg_status bdeg_item_range(bdeg_plan_t p, uint64_t item, uint64_t *begin, uint64_t *end) {
     if (!p || !begin || !end) return fail(p, BDEG_E_INVALID, "NULL argument");
-    if (p->K == 0 || item >= p->nblocks) return fail(p, BDEG_E_INVALID, "item out of range");
-    // colex unrank of the item over D-subsets of {0..N-K+D-1}, shifted by K-D
-    const int D = p->D, kd = p->K - p->D;
-    uint64_t r = item, base = 0;
-    int first = p->N;
-    for (int t = D - 1; t >= 0; --t) {
-        int u = t;
-        while (C(p->binom, u + 1, t + 1) <= r) ++u;
-        r -= C(p->binom, u, t + 1);
-        base += C(p->binom, u + kd, kd + t + 1);
-        if (t == 0) first = u + kd;
-    }
+    if (p->K == 0 || p->big || item >= p->nitems) return fail(p, BDEG_E_INVALID, "item out of range");
+    int d = 0;
+    std::vector<int> top;
+    decode_position(p, item, d, top);
+    const int kd = p->K - d;
+    uint64_t base = 0;
+    for (int t = 0; t < d; ++t) base += C(p->binom, top[t], kd + t + 1);
     *begin = base;
-    *end = base + C(p->binom, first, kd);
+    *end = base + C(p->binom, d > 0 ? top[0] : p->N, kd);
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_queue_info(bdeg_plan_t p, uint64_t *n_items, uint64_t *n_split, uint64_t *n_static,
+                            uint64_t *grab) {
+    if (!p) return fail(p, BDEG_E_INVALID, "NULL plan");
+    const bool k = p->K > 0 && !p->big;
+    if (n_items) *n_items = k ? p->nitems : 0;
+    if (n_split) *n_split = k ? p->split.size() : 0;
+    if (n_static) *n_static = k ? p->nstatic_steal : 0;
+    if (grab) *grab = k ? p->grab : 0;
     return BDEG_OK;
 }
 
@@ -1363,6 +1605,36 @@ bdeg_status bdeg_dimension_modp(int32_t n, int32_t m, const int64_t *A, int32_t 
         best = std::max(best, r);
     }
     *dim = (int32_t)(n - best);
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_smith_gpu(int32_t n, int32_t m, const int64_t *A, int32_t device, void *stream, int64_t *rank,
+                           uint64_t *comp_lo, uint64_t *comp_hi, int64_t *unit_pivots) {
+    if (!A || !rank || n < 1 || m < 0) return fail(nullptr, BDEG_E_INVALID, "bad arguments");
+    for (size_t i = 0; i < (size_t)n * m; ++i)
+        if (A[i] >= ((int64_t)1 << 61) || A[i] <= -((int64_t)1 << 61))
+            return fail(nullptr, BDEG_E_TOO_LARGE, "matrix entry beyond 2^61");
+    long long piv = 0;
+    std::vector<int64_t> res;
+    int rr = 0, rc = 0;
+    if (m > 0) {
+        const int e = smith_unimodular(A, n, m, device, stream, &piv, res, rr, rc);
+        if (e < 0) return fail(nullptr, BDEG_E_CUDA, "GPU unimodular elimination failed (no CUDA device?)");
+        if (e > 0) return fail(nullptr, BDEG_E_TOO_LARGE, "unimodular elimination: an entry grew beyond 2^61");
+    }
+    int rres = 0;
+    u128 prod = 1;
+    if (rr > 0 && rc > 0) {
+        if ((double)rr * rc > 4.0e6)
+            return fail(nullptr, BDEG_E_TOO_LARGE, "residual block without unit pivots is too large (" +
+                                                       std::to_string(rr) + " x " + std::to_string(rc) + ")");
+        std::string err;
+        if (!smith_factors(rr, rc, res.data(), rres, prod, err)) return fail(nullptr, BDEG_E_TOO_LARGE, err);
+    }
+    *rank = piv + rres;
+    if (comp_lo) *comp_lo = (uint64_t)prod;
+    if (comp_hi) *comp_hi = (uint64_t)(prod >> 64);
+    if (unit_pivots) *unit_pivots = piv;
     return BDEG_OK;
 }
 

@@ -30,6 +30,10 @@ struct FrontEnd {
 bool analyze_system(int n, int m, const int64_t *A, const double *b_re, const double *b_im,
                     bool lll, FrontEnd &fe, std::string &err);
 
+// Invariant factors of a (small) integer matrix by the same Euclidean
+// Smith form: rank and |prod d_j|.  false + err on overflow.
+bool smith_factors(int n, int m, const int64_t *A, int &rank, u128 &prod, std::string &err);
+
 // Point configuration (Prop. 4; readings Z2/Z5): distinct non-zero
 // columns of P0 in first-occurrence order (min lifting on merge), then the
 // origin (generic case, K = d+1, v = (1, a)), or only the columns (homogeneous
@@ -63,16 +67,32 @@ struct DeviceProblem {
 struct LaunchArgs {
     DeviceProblem P;
     uint64_t rank_begin, rank_end;    // candidate colex ranks [begin, end)
-    uint64_t blk_first, blk_last;     // inclusive block-id range covering [begin, end)
-    uint64_t blk_offset, blk_stride;  // this GPU takes blocks blk_last - (offset + i*stride)
-    unsigned long long *counter;      // work-stealing counter (zeroed before launch)
+    // Work queue (bdeg_capi.cpp build_queue): positions [0, n_items).
+    //   mode 0 (rank range): position i = base-depth colex item blk_last - i
+    //   mode 1 (whole space, largest-first): positions < n_split are split
+    //     items (depth << 58 | colex id at that depth), the rest are grouped
+    //     base-depth items (group g: smallest top index grp_u[g], first
+    //     position n_split + grp_cum[g], members in colex order of the rest)
+    int mode;
+    uint64_t blk_first, blk_last;     // mode 0: inclusive base-depth item range covering [begin, end)
+    const uint64_t *split;            // mode 1
+    uint64_t n_split;
+    const uint64_t *grp_u, *grp_cum;  // mode 1: n_grp groups, grp_cum[n_grp] = grouped total
+    int n_grp;
+    uint64_t n_items;
+    uint64_t n_static;                // positions rank + i*world < n_static: static interleave
+    uint64_t grab;                    // tail positions taken per global atomic
+    int rank, world;
+    unsigned long long *counter;      // this GPU's queue counter (zeroed before launch)
+    unsigned long long *gcounter;     // cross-GPU tail counter (IPC-mapped) or null
     unsigned long long *slots;        // kNSlots accumulators
-    unsigned long long *ovf_queue;    // block ids whose int32-tier run overflowed
-    unsigned long long *ovf_count;
-    uint64_t ovf_cap;
+    unsigned long long *mark_bits;    // bitmap over queue positions: items this launch could not
+                                      // finish in its tier (narrow -> int64 -> int128 chain)
+    unsigned long long *replay_bits;  // replay launches: the positions to redo (cleared as read)
+    uint64_t ovf_words;               // 64-bit words of each bitmap
     int tier;                         // 0: int32/int32, 1: int32/int64 (bounds), 2: int64/int128
     int bits_v, bits_l;               // tier-1 bounds: |V| < 2^bits_v, |lift| < 2^bits_l
-    int replay;                       // 1: process ovf_queue[0..*ovf_count) in tier 2
+    int replay;                       // 1: process the positions set in replay_bits (tier 2 or 4)
     int grid, block;                  // launch shape
     int degree_only;                  // skip cell-dead subtrees
     unsigned long long *cells_out;    // optional (mask, |det|) output of the cells found
@@ -90,15 +110,19 @@ enum Slot {
     SLOT_CELLS = 4, SLOT_SINGULAR = 5, SLOT_CAND = 6, SLOT_TIES = 7,
     SLOT_OVF_BLOCKS = 8,   // int32-tier blocks queued for re-run
     SLOT_FATAL = 9,        // int64-tier overflow (value beyond int64)
-    SLOT_QFULL = 10,       // overflow queue exhausted
+    SLOT_QFULL = 10,       // (unused: the re-run bitmap has one bit per work item)
     SLOT_BLOCKS = 11, SLOT_UPDATES = 12, SLOT_LEAVES = 13,
-    SLOT_DEAD = 14         // leaves inside cell-dead subtrees (singular count only)
+    SLOT_DEAD = 14,        // leaves inside cell-dead subtrees (singular count only)
+    SLOT_WIDE = 15         // items re-run in the int128-value tier (tier 4)
 };
 
 // Dynamic shared memory bytes for a launch of the enumeration kernel.
 size_t enumerate_smem_bytes(int K, int N, int warps_per_cta);
 // Launch k_enumerate (returns cudaError_t as int).
 int launch_enumerate(const LaunchArgs &a);
+// Tier 4 (int128 values, 256-bit exact intermediates): replay of the items
+// marked in a.replay_bits by a tier-2 launch.
+int launch_enumerate_wide(const LaunchArgs &a);
 int kernel_warps_per_cta();
 // Max resident CTAs per SM for this configuration (occupancy API).
 int enumerate_max_ctas_per_sm(const LaunchArgs &a);
@@ -127,5 +151,7 @@ int launch_collect(const void *tab, const uint8_t *tags, uint64_t cap, uint8_t t
 
 // ---- front end at scale, bdeg_rank.cu
 long long rank_modp(const int64_t *A, int n, int m, uint32_t p, int device, void *stream);
+int smith_unimodular(const int64_t *A, int n, int m, int device, void *stream, long long *pivots,
+                     std::vector<int64_t> &residual, int &res_rows, int &res_cols);
 
 }  // namespace bdeg

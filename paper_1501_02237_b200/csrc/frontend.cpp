@@ -148,6 +148,28 @@ uint64_t derive_seed(uint64_t seed, int attempt) {
     return g.next();
 }
 
+bool smith_factors(int n, int m, const int64_t *A, int &rank, u128 &prod, std::string &err) {
+    try {
+        Mat M(n, std::vector<i128>(m)), P(n, std::vector<i128>(n, 0)), Q(m, std::vector<i128>(m, 0));
+        for (int i = 0; i < n; ++i) {
+            P[i][i] = 1;
+            for (int j = 0; j < m; ++j) M[i][j] = A[(size_t)i * m + j];
+        }
+        for (int j = 0; j < m; ++j) Q[j][j] = 1;
+        rank = smith_euclid(M, P, Q);
+        prod = 1;
+        for (int t = 0; t < rank; ++t) {
+            const i128 d = iabs(M[t][t]);
+            if (d != 0 && prod > (((u128)1 << 127) / (u128)d)) { err = "component count beyond 2^127"; return false; }
+            prod *= (u128)d;
+        }
+    } catch (const Overflow &) {
+        err = "Smith form of the residual: __int128 overflow";
+        return false;
+    }
+    return true;
+}
+
 bool analyze_system(int n, int m, const int64_t *A, const double *b_re, const double *b_im,
                     bool lll, FrontEnd &fe, std::string &err) {
     fe = FrontEnd();

@@ -185,4 +185,57 @@ def test_planner_tier_follows_value_sizes():
 
     assert tier(4, 12, 2, 1 << 10) == 0
     assert tier(4, 12, 2, 1 << 40) == 1
-    assert tier(6, 14, 1 << 20, 1 << 50) == 2
+    assert tier(6, 14, 1 << 12, 1 << 30) == 2
+    # V coordinates ~2^20 with a 2^50 lifting: lifted minors reach ~2^150,
+    # beyond the int128 tier; Hadamard's bound rejects the plan up front
+    with pytest.raises(B.BdegError) as ei:
+        tier(6, 14, 1 << 20, 1 << 50)
+    assert ei.value.status == B.bdeg.BDEG_E_TOO_LARGE and "Hadamard" in str(ei.value)
+
+
+def _warp_share(total, world, S, sms=148):
+    # the planner's assumption on a host without a GPU: 148 SMs, resident
+    # warps from k_enumerate's launch bounds (4 CTAs x 4 warps, 3 CTAs for S >= 5)
+    return total / (world * sms * (12 if S >= 5 else 16))
+
+
+@pytest.mark.parametrize("name", ["c5", "w26", "w27"])
+def test_work_queue_balance_at_world8(name):
+    """at world = 8 no work item exceeds a quarter of a warp's
+    share (items split one or more levels deeper), the queue is largest-first,
+    the static prefix holds ~80% of the candidates and the items still
+    partition the rank space (checked exhaustively for C5)."""
+    import bench
+    wl = bench.Workload(name)
+    plan = wl.plan(world=8, rank=3, device=0)
+    info = plan.info()
+    total = math.comb(info.N, info.K)
+    q = plan.queue_info()
+    share = _warp_share(total, 8, info.inner_levels)
+    sizes = {}
+    probe = {0, max(0, q["n_split"] - 1), q["n_split"], q["n_items"] - 1, q["n_static"] - 1}
+    for pos in probe:
+        if 0 <= pos < q["n_items"]:
+            b, e = plan.item_range(pos)
+            sizes[pos] = e - b
+    # the largest item is either the first split item or the first grouped one
+    biggest = max(sizes[0], sizes.get(q["n_split"], 0))
+    assert biggest <= share / 4, (name, biggest, share)
+    assert q["n_split"] > 0 or name == "w27"
+    if q["n_split"] > 0:
+        assert sizes[0] >= sizes[q["n_split"] - 1]            # split part sorted by size
+    # static prefix ~80% of the candidates: the interleave balances it
+    assert 0 < q["n_static"] <= q["n_items"] and q["grab"] >= 1
+    if name == "c5":
+        covered, ivs = 0, []
+        for pos in range(q["n_items"]):
+            b, e = plan.item_range(pos)
+            ivs.append((b, e))
+        ivs.sort()
+        assert ivs[0][0] == 0 and ivs[-1][1] == total
+        assert all(ivs[i][1] == ivs[i + 1][0] for i in range(len(ivs) - 1))
+        stat = sum(e - b for (b, e) in (plan.item_range(p) for p in range(q["n_static"])))
+        assert 0.75 * total <= stat <= 0.85 * total
+    # one GPU keeps the base depth (no split items): largest-first by group
+    q1 = wl.plan(world=1, device=0).queue_info()
+    assert q1["n_split"] == 0 and q1["n_static"] == q1["n_items"]

@@ -32,16 +32,22 @@ def _worker(rank, world, port, q):
     V, w = W.c5_points(1)
     plan = B.Plan.from_points(V, w, rank=rank, world=world, device=0)
     enable_work_stealing(plan, 0)
-    out = []
+    out, busy, mine = [], [], []
     for _ in range(3):                       # several steps: counters alternate by parity
         slots = torch.zeros(B.NSLOTS, dtype=torch.int64, device="cuda")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        e0.record()
         plan.degree_partial(slots.data_ptr())
+        e1.record()
         torch.cuda.synchronize()
+        busy.append(e0.elapsed_time(e1))
         host = slots.cpu()
+        mine.append(int(host[6]))            # candidates this rank enumerated
         all_reduce_slots(host)
         r = plan.finalize(host.tolist())
         out.append((r.degree, r.cells, r.singular, r.candidates))
-    q.put((rank, out))
+    q.put((rank, (out, busy, mine, plan.queue_info())))
     dist.destroy_process_group()
 
 
@@ -63,4 +69,13 @@ def test_two_ranks_share_one_queue():
     for p in procs:
         p.join(timeout=60)
     want = (full.degree, full.cells, full.singular, full.candidates)
-    assert all(step == want for r in (0, 1) for step in res[r])
+    assert all(step == want for r in (0, 1) for step in res[r][0])
+    # static share (~80% of the candidates, interleaved) + stealing tail: both
+    # ranks do a substantial part of every step, and their busy times are close
+    q0 = res[0][3]
+    assert q0["n_split"] > 0 and q0["n_static"] < q0["n_items"]
+    for s in range(3):
+        c0, c1 = res[0][2][s], res[1][2][s]
+        assert c0 + c1 == full.candidates and min(c0, c1) > 0.3 * full.candidates, (c0, c1)
+        b0, b1 = res[0][1][s], res[1][1][s]
+        print(f"step {s}: rank busy ms {b0:.3f} / {b1:.3f}, candidates {c0} / {c1}")

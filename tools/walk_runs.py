@@ -14,15 +14,13 @@ import paper_1501_02237_b200 as B  # noqa: E402
 
 torch.cuda.set_device(0)
 for wl in sys.argv[1].split(","):
-    desc, K, V, w, extra = bench.workload(wl)
     if wl.startswith("w"):   # the binomial system itself, generated lifting (basis-seeded if N > 64)
         import workloads as W
         A, b = W.master_space_system(int(wl[1]), int(wl[2]))
         p = B.Plan.from_system(A, b, seed=int(os.environ.get("WALK_SEED", "1")))
-        K, nv = p.info().K, p.info().N
     else:
-        p = B.Plan.from_points(V, w)
-        nv = len(V)
+        p = bench.Workload(wl).plan()
+    K, nv = p.info().K, p.info().N
     t0 = time.perf_counter()
     r = p.degree_walk()
     dt = time.perf_counter() - t0
