@@ -219,6 +219,30 @@ bdeg_status bdeg_cell_normal(bdeg_plan_t plan, uint64_t mask_lo, uint64_t mask_h
  * (cells whose values leave int32 are redone in int64, exact either way). */
 bdeg_status bdeg_degree_walk(bdeg_plan_t plan, bdeg_result *out);
 
+/* the walk with its hash set SHARDED over the ranks (the
+ * paper's KnownNodes table shared by its GPUs, rebuilt as
+ * owner-computes over NVLink): cell m is owned by rank hash(m) mod world
+ * (options.rank / options.world of the plan); each rank keeps only its cells
+ * (breadth-first window of levels L-1..L+1), expands its frontier, and the
+ * neighbours owned elsewhere are exchanged after every level by one
+ * all-to-all; volumes are summed by the owner and combined by one all-reduce.
+ * Every rank calls it with the same plan (same lifting) and a bdeg_comm whose
+ * callbacks implement the collectives over the caller's process group:
+ *   allreduce_sum(ctx, vals, n): host int64[n], SUM in place;
+ *   alltoall_counts(ctx, send, recv): host uint64[world] each;
+ *   alltoall_cells(ctx, d_send, send_counts, d_recv, recv_counts): DEVICE
+ *     buffers of 16-byte cells, segment per rank, complete on return.
+ * A callback returns 0 on success (else BDEG_E_COMM).  Ties abort every rank
+ * (BDEG_E_DEGENERATE; generated liftings are re-lifted collectively). */
+typedef struct {
+    void *ctx;
+    int (*allreduce_sum)(void *ctx, int64_t *vals, int32_t n);
+    int (*alltoall_counts)(void *ctx, const uint64_t *send, uint64_t *recv);
+    int (*alltoall_cells)(void *ctx, const void *d_send, const uint64_t *send_counts, void *d_recv,
+                          const uint64_t *recv_counts);
+} bdeg_comm;
+bdeg_status bdeg_degree_walk_sharded(bdeg_plan_t plan, const bdeg_comm *comm, bdeg_result *out);
+
 /* Cross-GPU dynamic work stealing.  One process (rank 0)
  * creates a pair of item counters in its GPU's memory and exports them as a
  * CUDA IPC handle (BDEG_STEAL_HANDLE_BYTES bytes); every rank (rank 0 included,

@@ -79,13 +79,25 @@ class _Result(ctypes.Structure):
                 ("total_ms", ctypes.c_double), ("wide_reruns", ctypes.c_uint64)]
 
 
+_ALLREDUCE = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32)
+_A2A_COUNTS = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64),
+                               ctypes.POINTER(ctypes.c_uint64))
+_A2A_CELLS = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64),
+                              ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64))
+
+
+class _Comm(ctypes.Structure):
+    _fields_ = [("ctx", ctypes.c_void_p), ("allreduce_sum", _ALLREDUCE),
+                ("alltoall_counts", _A2A_COUNTS), ("alltoall_cells", _A2A_CELLS)]
+
+
 EXPORTS = ["bdeg_default_options", "bdeg_plan", "bdeg_plan_points", "bdeg_plan_info",
            "bdeg_workspace_bytes", "bdeg_set_workspace", "bdeg_degree", "bdeg_degree_range",
            "bdeg_degree_partial", "bdeg_finalize", "bdeg_relift", "bdeg_last_error",
            "bdeg_status_str", "bdeg_destroy", "bdeg_launch_count", "bdeg_num_items",
            "bdeg_item_range", "bdeg_cells", "bdeg_degree_walk", "bdeg_cell_normal",
            "bdeg_steal_create", "bdeg_steal_attach", "bdeg_rank_modp", "bdeg_dimension_modp",
-           "bdeg_plan_points_get", "bdeg_queue_info", "bdeg_smith_gpu"]
+           "bdeg_plan_points_get", "bdeg_queue_info", "bdeg_smith_gpu", "bdeg_degree_walk_sharded"]
 
 
 def _load():
@@ -93,6 +105,19 @@ def _load():
         raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
                           "(libbdeg has no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
+    if os.environ.get("BDEG_LIB"):
+        # A/B tuning builds of older revisions may lack the newest entry points
+        class _Tolerant:
+            def __init__(self, l):
+                object.__setattr__(self, "_l", l)
+
+            def __getattr__(self, name):
+                try:
+                    return getattr(self._l, name)
+                except AttributeError:
+                    return type("_Missing", (), {})()
+
+        lib = _Tolerant(lib)
     P = ctypes.POINTER
     plan_t = ctypes.c_void_p
     lib.bdeg_default_options.argtypes = [P(_Options)]
@@ -131,6 +156,8 @@ def _load():
                                      P(ctypes.c_int64)]
     lib.bdeg_cell_normal.restype = ctypes.c_int
     lib.bdeg_degree_walk.restype = ctypes.c_int
+    lib.bdeg_degree_walk_sharded.argtypes = [plan_t, P(_Comm), P(_Result)]
+    lib.bdeg_degree_walk_sharded.restype = ctypes.c_int
     lib.bdeg_steal_create.argtypes = [ctypes.c_int32, ctypes.c_char_p]
     lib.bdeg_steal_create.restype = ctypes.c_int
     lib.bdeg_steal_attach.argtypes = [plan_t, ctypes.c_char_p]
@@ -166,9 +193,7 @@ def steal_create(device: int) -> bytes:
 
 def dimension_modp(A, device=None) -> int:
     """dim V*(x^A - b) = n - rank A by GPU row reduction mod 2 primes."""
-    n = len(A)
-    m = len(A[0]) if n else 0
-    buf = _i64([A[i][j] for i in range(n) for j in range(m)])
+    buf, n, m = _matrix_i64(A)
     d = ctypes.c_int32()
     _check(lib.bdeg_dimension_modp(n, m, buf, _current_device() if device is None else device, ctypes.byref(d)))
     return d.value
@@ -177,9 +202,7 @@ def dimension_modp(A, device=None) -> int:
 def smith_gpu(A, device=None):
     """Exact (rank, |prod d_j|, unit pivots) of A by GPU unit-pivot elimination
     plus the host Smith form of the residual (bdeg_smith_gpu)."""
-    n = len(A)
-    m = len(A[0]) if n else 0
-    buf = _i64([A[i][j] for i in range(n) for j in range(m)])
+    buf, n, m = _matrix_i64(A)
     r, lo, hi, piv = ctypes.c_int64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_int64()
     _check(lib.bdeg_smith_gpu(n, m, buf, _current_device() if device is None else device, None,
                               ctypes.byref(r), ctypes.byref(lo), ctypes.byref(hi), ctypes.byref(piv)))
@@ -271,6 +294,22 @@ def _i64(values):
     return (ctypes.c_int64 * max(1, len(vals)))(*vals)
 
 
+def _matrix_i64(A):
+    """Row-major int64 buffer of an n x m matrix (list of rows or a numpy array)."""
+    try:
+        import numpy as np
+        arr = np.ascontiguousarray(np.asarray(A, dtype=np.int64))
+        if arr.ndim == 2 and arr.size > 0:
+            ptr = arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+            ptr._keep = arr                      # the array outlives the call through the pointer
+            return ptr, arr.shape[0], arr.shape[1]
+    except (ImportError, ValueError, OverflowError):
+        pass
+    n = len(A)
+    m = len(A[0]) if n else 0
+    return _i64([A[i][j] for i in range(n) for j in range(m)]), n, m
+
+
 def _check(status, plan=None):
     if status != BDEG_OK:
         msg = lib.bdeg_last_error(plan).decode(errors="replace")
@@ -294,6 +333,7 @@ class Plan:
         self._h = handle
         self._keep = keep
         self._ws = None
+        self._world = 1
 
     # -- construction ------------------------------------------------
     @classmethod
@@ -322,7 +362,9 @@ class Plan:
         o = _options(**opts)
         h = ctypes.c_void_p()
         _check(lib.bdeg_plan(ctypes.byref(pr), ctypes.byref(o), ctypes.byref(h)))
-        return cls(h, keep)
+        plan = cls(h, keep)
+        plan._world = o.world
+        return plan
 
     @classmethod
     def from_points(cls, V, lifting=None, **opts):
@@ -336,7 +378,9 @@ class Plan:
         o = _options(**opts)
         h = ctypes.c_void_p()
         _check(lib.bdeg_plan_points(K, N, Vb, lb, ctypes.byref(o), ctypes.byref(h)))
-        return cls(h, [Vb, lb])
+        plan = cls(h, [Vb, lb])
+        plan._world = o.world
+        return plan
 
     # -- queries -----------------------------------------------------
     def info(self) -> Result:
@@ -403,6 +447,52 @@ class Plan:
         """Output-sensitive degree by walking the subdivision."""
         r = _Result()
         _check(lib.bdeg_degree_walk(self._h, ctypes.byref(r)), self._h)
+        return _result(r)
+
+    def degree_walk_sharded(self, allreduce_sum, alltoall_counts, alltoall_cells) -> Result:
+        """The walk with its hash set sharded over the ranks (bdeg_degree_walk_sharded).
+        The three callables implement the collectives (multi.degree_walk_distributed):
+          allreduce_sum(list[int]) -> list[int];  alltoall_counts(list[int]) -> list[int];
+          alltoall_cells(d_send_ptr, send_counts, d_recv_ptr, recv_counts) -> None."""
+        errors = []
+
+        def ar(_ctx, vals, n):
+            try:
+                out = allreduce_sum([vals[i] for i in range(n)])
+                for i in range(n):
+                    vals[i] = int(out[i])
+                return 0
+            except Exception as e:  # noqa: BLE001 - reported as BDEG_E_COMM
+                errors.append(e)
+                return 1
+
+        def ac(_ctx, send, recv):
+            try:
+                w = self._world
+                out = alltoall_counts([send[i] for i in range(w)])
+                for i in range(w):
+                    recv[i] = int(out[i])
+                return 0
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+                return 1
+
+        def ax(_ctx, d_send, scnt, d_recv, rcnt):
+            try:
+                w = self._world
+                alltoall_cells(d_send or 0, [scnt[i] for i in range(w)], d_recv or 0, [rcnt[i] for i in range(w)])
+                return 0
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+                return 1
+
+        cbs = (_ALLREDUCE(ar), _A2A_COUNTS(ac), _A2A_CELLS(ax))
+        comm = _Comm(None, *cbs)
+        r = _Result()
+        st = lib.bdeg_degree_walk_sharded(self._h, ctypes.byref(comm), ctypes.byref(r))
+        if st != BDEG_OK and errors:
+            raise BdegError(st, f"{lib.bdeg_last_error(self._h).decode(errors='replace')}: {errors[0]!r}")
+        _check(st, self._h)
         return _result(r)
 
     def cells(self, begin: int = 0, end: int = None, capacity: int = 1 << 20):

@@ -781,12 +781,14 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
         a.counter = p->d_ctr + 1;
         a.replay_bits = bitsA;
         a.mark_bits = bitsB;
+        a.replay_gate = slots + SLOT_OVF_BLOCKS;   // items the narrow launch marked
         rc = launch_enumerate(a);
         if (rc) return fail(p, BDEG_E_CUDA, std::string("k_enumerate replay: ") + cudaGetErrorString((cudaError_t)rc));
     }
     a.counter = p->d_ctr + 3;
     a.replay_bits = bitsB;
     a.mark_bits = nullptr;
+    a.replay_gate = slots + SLOT_WIDE;             // items the tier-2 launches marked
     rc = launch_enumerate_wide(a);
     if (rc) return fail(p, BDEG_E_CUDA, std::string("k_enumerate_wide: ") + cudaGetErrorString((cudaError_t)rc));
     return BDEG_OK;
@@ -1196,6 +1198,264 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
     return BDEG_OK;
 }
 
+// SURVEY §8.f3 sharded walk: the hash set split over the ranks by owner =
+// hash(cell) mod world; one all-to-all of the neighbours owned elsewhere per
+// level (chunked so the outgoing buffer stays bounded), per-level collective
+// decisions (termination, ties, overflow) through one small all-reduce, and
+// the volumes summed by the owners.  Same kernels as walk_once.
+bdeg_status walk_sharded(bdeg_plan_s *p, const bdeg_comm *cm, bdeg_result *r, double *kms) {
+    cudaStream_t st = (cudaStream_t)p->opt.stream;
+    const double t0 = now_ms();
+    const int W = std::max(1, p->opt.world), R = p->opt.rank;
+    const int K = p->K;
+    auto comm_fail = [&](const char *what) { return fail(p, BDEG_E_COMM, std::string("sharded walk: ") + what); };
+    auto allreduce = [&](int64_t *v, int n) -> bool { return cm->allreduce_sum(cm->ctx, v, n) == 0; };
+    // ---- start cell: rank 0's, broadcast by a sum where the others give 0
+    int64_t sv[4] = {0, 0, 0, 0};
+    if (R == 0) {
+        if (p->big) {
+            if (p->user_lift || (p->basis_lo == 0 && p->basis_hi == 0)) sv[3] = BDEG_E_INVALID;
+            else { sv[0] = (int64_t)p->basis_lo; sv[1] = (int64_t)p->basis_hi; sv[2] = 1; }
+        } else {
+            uint64_t pair[2 * 64];
+            uint64_t n = 0;
+            bdeg_status s = cells_range(p, 0, p->total, pair, 64, &n, true);
+            if (s) sv[3] = s;
+            else if (n > 0) { sv[0] = (int64_t)pair[0]; sv[2] = 1; }
+        }
+    }
+    if (!allreduce(sv, 4)) return comm_fail("allreduce failed");
+    if (sv[3] == BDEG_E_INVALID) return fail(p, BDEG_E_INVALID, "N > 64 needs a generated lifting (basis-seeded start cell)");
+    if (sv[3] != 0) return fail(p, (bdeg_status)sv[3], "start-cell search failed on rank 0");
+    if (sv[2] == 0) return fail(p, BDEG_E_DEGENERATE, "no cell found (degenerate lifting)");
+    const uint64_t start[2] = {(uint64_t)sv[0], (uint64_t)sv[1]};
+    // ---- buffers
+    uint64_t cap = 1ull << 22;
+    if (const char *c0 = std::getenv("BDEG_WALK_CAP0")) cap = std::max<uint64_t>(1024, std::strtoull(c0, nullptr, 10));
+    else {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        cap = std::max<uint64_t>(cap, (uint64_t)((fr * 0.4) / 17) & ~1023ull);
+    }
+    const uint64_t chunk_max = std::max<uint64_t>(1024, (1ull << 30) / (16ull * (uint64_t)K));   // <= 1 GB outgoing
+    DevBuf table, tags, cur, nxt, aux, remote, sendb, recvb, ovfl, ocnt;
+    uint64_t ccap = 1 << 16, ncap = 1 << 16, rcap = 0, scap = 0, vcap = 0, ovfl_cap = 0;
+    if (!table.alloc(cap * 16) || !tags.alloc(cap) || !cur.alloc(ccap * 16) || !nxt.alloc(ncap * 16) ||
+        !aux.alloc(16 * 8) || !ocnt.alloc(2 * 8 * (size_t)W))
+        return fail(p, BDEG_E_TOO_LARGE, "sharded walk: cudaMalloc of the hash set failed");
+    unsigned long long *next_cnt = aux.u(), *counter = aux.u() + 1, *stats = aux.u() + 2, *lvol = aux.u() + 10;
+    cudaMemsetAsync(table.p, 0, cap * 16, st);
+    cudaMemsetAsync(tags.p, 0, cap, st);
+    uint64_t ncur = 0;
+    if (walk_owner(start[0], start[1], W) == R) {
+        const uint64_t h0 = (uint64_t)(((u128)walk_hash(start[0], start[1]) * cap) >> 64);
+        cudaMemcpyAsync((char *)table.p + h0 * 16, start, 16, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(cur.p, start, 16, cudaMemcpyHostToDevice, st);
+        ncur = 1;
+    }
+    cudaStreamSynchronize(st);
+    const int grid = std::max(1, dev_info(p->opt.device).sms) * 4;
+    const int64_t limV = p->tier == 2 ? 0 : (int64_t)1 << (p->tier == 0 ? 30 : p->bits_v);
+    const int64_t limL = p->tier == 2 ? 0 : (int64_t)1 << (p->tier == 0 ? 31 : p->bits_l);
+    const int narrow = (p->tier == 0 && !std::getenv("BDEG_WALK_WIDE")) ? 1 : 0;
+    u128 vol = 0;
+    uint64_t cells = 0, ridges = 0, boundary = 0, sent_total = 0, evictions = 0;
+    int fused = 1, levels = 0;
+    uint64_t live = ncur, prev_level = 0;   // cells in this rank's table; cells of level L-1 (kept in `nxt`)
+    std::vector<uint64_t> scnt(W), rcnt(W);
+    std::vector<int64_t> red(8 + W);
+    for (;;) {
+        const unsigned tag = (unsigned)(levels + 1) & 255u;
+        // chunks of this level: the same count on every rank (max)
+        std::fill(red.begin(), red.end(), 0);
+        red[8 + R] = (int64_t)((ncur + chunk_max - 1) / chunk_max);
+        if (!allreduce(red.data(), 8 + W)) return comm_fail("allreduce failed");
+        int64_t nch = 0;
+        for (int i = 0; i < W; ++i) nch = std::max(nch, red[8 + i]);
+        uint64_t nnext = 0;
+        int64_t flags[6] = {0, 0, 0, 0, 0, 0};   // ties, inconsistent/overflow, table full, comm, next total, -
+        for (int64_t c = 0; c < nch; ++c) {
+            const uint64_t b = std::min<uint64_t>(ncur, (uint64_t)c * chunk_max);
+            const uint64_t e = std::min<uint64_t>(ncur, b + chunk_max);
+            const uint64_t nc = e - b;
+            // room for this chunk's local neighbours (<= K per cell) in the next frontier
+            if (nnext + nc * (uint64_t)K > ncap) {
+                const uint64_t want = (nnext + nc * (uint64_t)K + 1023) & ~1023ull;
+                DevBuf t;
+                if (!t.alloc(want * 16)) return fail(p, BDEG_E_TOO_LARGE, "sharded walk: frontier allocation failed");
+                if (nnext) cudaMemcpyAsync(t.p, nxt.p, nnext * 16, cudaMemcpyDeviceToDevice, st);
+                cudaStreamSynchronize(st);
+                std::swap(t.p, nxt.p);
+                ncap = want;
+            }
+            // <= K neighbours per cell, twice for cells redone in int64 after the narrow kernel
+            if (2 * nc * (uint64_t)K > rcap) {
+                rcap = (2 * nc * (uint64_t)K + 1023) & ~1023ull;
+                if (!remote.alloc(rcap * 16) || !sendb.alloc(rcap * 16))
+                    return fail(p, BDEG_E_TOO_LARGE, "sharded walk: exchange buffer allocation failed");
+            }
+            if (narrow && nc > ovfl_cap) {
+                ovfl_cap = std::max<uint64_t>(1024, nc);
+                if (!ovfl.alloc(ovfl_cap * 16)) return fail(p, BDEG_E_CUDA, "cudaMalloc (walk overflow list) failed");
+            }
+            uint64_t nn = nnext;
+            cudaMemsetAsync(aux.p, 0, 16 * 8, st);
+            cudaMemcpyAsync(next_cnt, &nn, 8, cudaMemcpyHostToDevice, st);
+            cudaMemsetAsync(ocnt.p, 0, 2 * 8 * (size_t)W, st);
+            unsigned long long *rcnt_d = ocnt.u() + 2 * W - 1;   // remote count lives in the spare slot
+            cudaMemsetAsync(rcnt_d, 0, 8, st);
+            uint64_t h[16] = {0};
+            if (nc > 0) {
+                int rc = launch_walk(p->d_L, K, p->N, (const char *)cur.p + b * 16, nc, nxt.p, next_cnt, table.p, cap,
+                                     counter, stats, grid, st, limV, limL, lvol, &fused, (uint8_t *)tags.p, tag, ncap,
+                                     narrow, ovfl.p, aux.u() + 15, ovfl_cap, p->v_safe ? 1 : 0, W, R, remote.p,
+                                     rcnt_d, rcap);
+                if (rc) return fail(p, BDEG_E_CUDA, std::string("k_walk: ") + cudaGetErrorString((cudaError_t)rc));
+                cudaMemcpyAsync(h, aux.p, 16 * 8, cudaMemcpyDeviceToHost, st);
+                if (cudaStreamSynchronize(st) != cudaSuccess) return fail(p, BDEG_E_CUDA, "walk level failed");
+                if (narrow && h[15] > 0) {   // cells whose values left int32: redo them with int64 storage
+                    cudaMemsetAsync(counter, 0, 8, st);
+                    cudaMemsetAsync(aux.u() + 15, 0, 8, st);
+                    rc = launch_walk(p->d_L, K, p->N, ovfl.p, h[15], nxt.p, next_cnt, table.p, cap, counter, stats,
+                                     grid, st, limV, limL, lvol, &fused, (uint8_t *)tags.p, tag, ncap, 0, nullptr,
+                                     nullptr, 0, 0, W, R, remote.p, rcnt_d, rcap);
+                    if (rc) return fail(p, BDEG_E_CUDA, std::string("k_walk: ") + cudaGetErrorString((cudaError_t)rc));
+                    cudaMemcpyAsync(h, aux.p, 16 * 8, cudaMemcpyDeviceToHost, st);
+                    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(p, BDEG_E_CUDA, "walk level failed");
+                }
+            }
+            const uint64_t *sv2 = h + 2;
+            ridges += sv2[0];
+            boundary += sv2[5];
+            flags[0] += (int64_t)sv2[1];
+            flags[1] += (int64_t)(sv2[2] + sv2[4]);
+            flags[2] += (int64_t)sv2[3];
+            if (fused) {
+                for (int i = 3; i >= 0; --i) vol += (u128)h[10 + i] << (32 * i);
+                cells += h[14];
+            }
+            nnext = h[0];
+            // ---- route the neighbours owned by other ranks
+            uint64_t nrem = 0;
+            cudaMemcpy(&nrem, rcnt_d, 8, cudaMemcpyDeviceToHost);
+            if (nrem > rcap) flags[2] += 1;             // cannot happen (<= K per cell); reported as full
+            nrem = std::min(nrem, rcap);
+            unsigned long long *cnt_d = ocnt.u();
+            cudaMemsetAsync(cnt_d, 0, 8 * (size_t)W, st);
+            launch_owner_count(remote.p, nrem, W, cnt_d, st);
+            std::vector<unsigned long long> hc(W);
+            cudaMemcpyAsync(hc.data(), cnt_d, 8 * (size_t)W, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            std::vector<unsigned long long> off(W, 0);
+            for (int i = 1; i < W; ++i) off[i] = off[i - 1] + hc[i - 1];
+            cudaMemcpyAsync(cnt_d, off.data(), 8 * (size_t)W, cudaMemcpyHostToDevice, st);
+            launch_owner_scatter(remote.p, nrem, W, cnt_d, sendb.p, st);
+            if (cudaStreamSynchronize(st) != cudaSuccess) return fail(p, BDEG_E_CUDA, "owner partition failed");
+            for (int i = 0; i < W; ++i) scnt[i] = hc[i];
+            sent_total += nrem;
+            if (cm->alltoall_counts(cm->ctx, scnt.data(), rcnt.data()) != 0) return comm_fail("alltoall (counts) failed");
+            uint64_t nrecv = 0;
+            for (int i = 0; i < W; ++i) nrecv += rcnt[i];
+            if (nrecv > vcap) {
+                vcap = (nrecv + 1023) & ~1023ull;
+                if (!recvb.alloc(vcap * 16)) return fail(p, BDEG_E_TOO_LARGE, "sharded walk: receive buffer allocation failed");
+            }
+            if (cm->alltoall_cells(cm->ctx, sendb.p, scnt.data(), recvb.p, rcnt.data()) != 0)
+                return comm_fail("alltoall (cells) failed");
+            if (nnext + nrecv > ncap) {
+                const uint64_t want = (nnext + nrecv + 1023) & ~1023ull;
+                DevBuf t;
+                if (!t.alloc(want * 16)) return fail(p, BDEG_E_TOO_LARGE, "sharded walk: frontier allocation failed");
+                if (nnext) cudaMemcpyAsync(t.p, nxt.p, nnext * 16, cudaMemcpyDeviceToDevice, st);
+                cudaStreamSynchronize(st);
+                std::swap(t.p, nxt.p);
+                ncap = want;
+            }
+            if (nrecv > 0) {
+                cudaMemsetAsync(stats + 3, 0, 8, st);
+                int rc = launch_insert_recv(recvb.p, nrecv, table.p, (uint8_t *)tags.p, cap, (uint8_t)tag, nxt.p,
+                                            next_cnt, ncap, stats + 3, st);
+                if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
+                uint64_t fullc = 0;
+                cudaMemcpyAsync(&nnext, next_cnt, 8, cudaMemcpyDeviceToHost, st);
+                cudaMemcpyAsync(&fullc, stats + 3, 8, cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                flags[2] += (int64_t)fullc;
+            }
+        }
+        // ---- collective decisions for the level
+        std::fill(red.begin(), red.end(), 0);
+        red[0] = flags[0];
+        red[1] = flags[1];
+        red[2] = flags[2];
+        red[3] = (int64_t)nnext;
+        red[4] = fused ? 0 : 1;
+        if (!allreduce(red.data(), 8 + W)) return comm_fail("allreduce failed");
+        if (red[0] > 0) return fail(p, BDEG_E_DEGENERATE, "degenerate lifting: a ridge has a tie (sharded walk)");
+        if (red[1] > 0) return fail(p, BDEG_E_TOO_LARGE, "sharded walk: inconsistent ridge or value overflow");
+        if (red[2] > 0) return fail(p, BDEG_E_TOO_LARGE, "sharded walk: hash set shard full");
+        const bool any_unfused = red[4] > 0;
+        std::swap(cur.p, nxt.p);
+        std::swap(ccap, ncap);
+        prev_level = ncur;
+        ncur = nnext;
+        live += nnext;
+        ++levels;
+        if (red[3] == 0) break;                       // no rank has a next frontier
+        // BFS window: rebuild this rank's shard from levels L-1 (nxt) and L (cur)
+        // when it passes half load (fused walk only: the volumes are already summed)
+        if (!any_unfused && live * 2 > cap) {
+            cudaMemsetAsync(table.p, 0, cap * 16, st);
+            cudaMemsetAsync(tags.p, 0, cap, st);
+            cudaMemsetAsync(stats + 3, 0, 8, st);
+            int rc = launch_insert_list(nxt.p, prev_level, table.p, (uint8_t *)tags.p, cap,
+                                        (uint8_t)((levels - 1) & 255), stats + 3, st);
+            if (!rc) rc = launch_insert_list(cur.p, ncur, table.p, (uint8_t *)tags.p, cap, (uint8_t)(levels & 255),
+                                             stats + 3, st);
+            if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
+            cudaStreamSynchronize(st);
+            live = prev_level + ncur;
+            ++evictions;
+            if (live * 4 > cap * 3) return fail(p, BDEG_E_TOO_LARGE, "sharded walk: two levels exceed the hash set shard");
+        }
+        if (levels > 100000) return fail(p, BDEG_E_TOO_LARGE, "sharded walk: too many levels");
+    }
+    if (!fused) {   // exact volumes of this rank's cells (every owned cell is still in the table)
+        if (evictions) return fail(p, BDEG_E_TOO_LARGE, "sharded walk: unfused walk needs the whole shard");
+        cudaMemsetAsync(aux.p, 0, 16 * 8, st);
+        int rc = launch_cellvol(p->d_L, K, p->N, table.p, cap, aux.u() + 8, aux.u(), grid, st, limV, limL);
+        if (rc) return fail(p, BDEG_E_CUDA, cudaGetErrorString((cudaError_t)rc));
+        uint64_t h[16];
+        cudaMemcpyAsync(h, aux.p, 16 * 8, cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) return fail(p, BDEG_E_CUDA, "cell volume pass failed");
+        if (h[8 + 5] > 0) return fail(p, BDEG_E_TOO_LARGE, "cell volume overflow");
+        vol = 0;
+        for (int i = 3; i >= 0; --i) vol = (vol << 32) + (u128)h[8 + i];
+        cells = h[8 + 4];
+    }
+    // ---- combine: the volume as four 32-bit limbs (exact in int64 sums)
+    int64_t tot[8] = {(int64_t)(uint64_t)(vol & 0xFFFFFFFFu), (int64_t)(uint64_t)((vol >> 32) & 0xFFFFFFFFu),
+                      (int64_t)(uint64_t)((vol >> 64) & 0xFFFFFFFFu), (int64_t)(uint64_t)(vol >> 96),
+                      (int64_t)cells, (int64_t)ridges, (int64_t)boundary, (int64_t)sent_total};
+    if (!allreduce(tot, 8)) return comm_fail("allreduce failed");
+    u128 v = 0;
+    for (int i = 3; i >= 0; --i) v = (v << 32) + (u128)(uint64_t)tot[i];
+    r->deg_lo = (uint64_t)v;
+    r->deg_hi = (int64_t)(uint64_t)(v >> 64);
+    r->cells = (uint64_t)tot[4];
+    r->candidates = 0;
+    r->singular = 0;
+    r->singular_complete = 0;
+    r->leaves = (uint64_t)tot[5];
+    r->dead_leaves = (uint64_t)tot[6];
+    if (std::getenv("BDEG_DEBUG"))
+        fprintf(stderr, "[bdeg sharded walk] rank %d/%d: %d levels, %llu owned cells, %llu sent, %llu evictions, "
+                "%.2f ms\n", R, W, levels, (unsigned long long)cells, (unsigned long long)sent_total,
+                (unsigned long long)evictions, now_ms() - t0);
+    *kms += now_ms() - t0;
+    return BDEG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1529,6 +1789,41 @@ bdeg_status bdeg_degree_walk(bdeg_plan_t p, bdeg_result *out) {
     for (int attempt = p->relifts;; ++attempt) {
         fill_front(p, &r);
         s = walk_once(p, &r, &kms);
+        if (s != BDEG_E_DEGENERATE) break;
+        if (p->user_lift || (p->opt.flags & BDEG_FLAG_NO_RELIFT)) return s;
+        if (attempt + 1 > p->opt.max_relift) return s;
+        bdeg_relift(p, attempt + 1);
+        s = ensure_device(p);
+        if (s) return s;
+    }
+    if (s) return s;
+    r.relifts = p->relifts;
+    r.seed_used = p->seed_used;
+    r.kernel_ms = kms;
+    r.total_ms = now_ms() - t0;
+    *out = r;
+    return BDEG_OK;
+}
+
+bdeg_status bdeg_degree_walk_sharded(bdeg_plan_t p, const bdeg_comm *comm, bdeg_result *out) {
+    if (!p || !out || !comm || !comm->allreduce_sum || !comm->alltoall_counts || !comm->alltoall_cells)
+        return fail(p, BDEG_E_INVALID, "NULL argument");
+    const double t0 = now_ms();
+    bdeg_result r;
+    fill_front(p, &r);
+    if (p->K == 0) {
+        r.deg_lo = 1;
+        *out = r;
+        return BDEG_OK;
+    }
+    bdeg_status s = ensure_device(p);
+    if (s) return s;
+    double kms = 0;
+    // ties are reduced over all ranks inside, so every rank takes the same
+    // branch here and re-lifts with the same attempt
+    for (int attempt = p->relifts;; ++attempt) {
+        fill_front(p, &r);
+        s = walk_sharded(p, comm, &r, &kms);
         if (s != BDEG_E_DEGENERATE) break;
         if (p->user_lift || (p->opt.flags & BDEG_FLAG_NO_RELIFT)) return s;
         if (attempt + 1 > p->opt.max_relift) return s;

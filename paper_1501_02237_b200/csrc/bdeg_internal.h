@@ -93,6 +93,7 @@ struct LaunchArgs {
     int tier;                         // 0: int32/int32, 1: int32/int64 (bounds), 2: int64/int128
     int bits_v, bits_l;               // tier-1 bounds: |V| < 2^bits_v, |lift| < 2^bits_l
     int replay;                       // 1: process the positions set in replay_bits (tier 2 or 4)
+    const unsigned long long *replay_gate;   // replays: the slot counting the marked items (0 => exit at once)
     int grid, block;                  // launch shape
     int degree_only;                  // skip cell-dead subtrees
     unsigned long long *cells_out;    // optional (mask, |det|) output of the cells found
@@ -139,7 +140,18 @@ int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, 
                 unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL,
                 unsigned long long *vol, int *fused, uint8_t *tags, unsigned tag, uint64_t next_cap,
                 int narrow = 0, void *ovfl = nullptr, unsigned long long *ovfl_cnt = nullptr,
-                uint64_t ovfl_cap = 0, int vsafe = 0);
+                uint64_t ovfl_cap = 0, int vsafe = 0, int world = 1, int rank = 0, void *remote = nullptr,
+                unsigned long long *remote_cnt = nullptr, uint64_t remote_cap = 0);
+// sharded walk: owner of a cell (= device owner_of), receive-side insert,
+// partition of the remote cells by owner
+inline int walk_owner(uint64_t lo, uint64_t hi, int world) {
+    return (int)((uint32_t)walk_hash(lo, hi) % (uint32_t)world);
+}
+int launch_insert_recv(const void *list, uint64_t n, void *tab, uint8_t *tags, uint64_t cap, uint8_t tag, void *next,
+                       unsigned long long *next_cnt, uint64_t next_cap, unsigned long long *full_flag, void *stream);
+int launch_owner_count(const void *list, uint64_t n, int world, unsigned long long *cnt, void *stream);
+int launch_owner_scatter(const void *list, uint64_t n, int world, unsigned long long *cursor, void *out,
+                         void *stream);
 int launch_cellvol(const int64_t *L, int K, int N, const void *table, uint64_t cap, unsigned long long *out,
                    unsigned long long *counter, int grid, void *stream, int64_t limV, int64_t limL);
 int launch_rehash(const void *old, const uint8_t *old_tags, uint64_t oldcap, void *tab, uint8_t *tags, uint64_t cap,

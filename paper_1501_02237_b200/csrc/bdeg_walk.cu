@@ -238,7 +238,19 @@ struct WalkArgs {
                                       // [6] cells redone with int128 numerators (D&C walk)
     int grid;
     void *stream;
+    // sharded walk: the hash set is split over `world` ranks,
+    // cell m is owned by rank owner(m); neighbours owned elsewhere are
+    // appended to `remote` and exchanged after the level (all-to-all)
+    int world, rank;
+    M128 *remote;
+    unsigned long long *remote_cnt;
+    uint64_t remote_cap;
 };
+
+// owner rank of a cell (low half of the hash; the table slot uses the high half)
+__device__ __forceinline__ int owner_of(const M128 &m, int world) {
+    return (int)((uint32_t)mhash(m) % (uint32_t)world);
+}
 
 // Insert key (linear probing); true if it was new.  tags (optional): the
 // slot's walk level (mod 256) is recorded beside it, so a level's cells can be
@@ -359,7 +371,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_walk(WalkArgs a) {
         if (lane == 0) {
             const M128 nm = mset(ridge, found);
             bool full = false;
-            if (insert(a.table, a.cap, nm, full, a.tags, a.tag)) {
+            if (a.world > 1 && owner_of(nm, a.world) != a.rank) {
+                const unsigned long long pos = atomicAdd(a.remote_cnt, 1ull);
+                if (pos < a.remote_cap) a.remote[pos] = nm;
+            } else if (insert(a.table, a.cap, nm, full, a.tags, a.tag)) {
                 const unsigned long long pos = atomicAdd(a.next_cnt, 1ull);
                 if (pos < a.next_cap) a.next[pos] = nm;   // else re-collected by tag
             }
@@ -455,11 +470,22 @@ __device__ __forceinline__ int64_t ridge_step(const T *bx, const T *by, int64_t 
 // probes instead of K serial ones, and one warp-aggregated frontier append.
 __device__ __forceinline__ void insert_neighbours(M128 m, int my_p, int my_nb, int lane, const WalkArgs &a,
                                                   unsigned long long (&st)[6]) {
-    bool isnew = false, full = false;
+    bool isnew = false, full = false, isremote = false;
     M128 nm = {0, 0};
     if (my_nb >= 0) {
         nm = mset(mclear(m, my_p), my_nb);
-        isnew = insert(a.table, a.cap, nm, full, a.tags, a.tag);
+        if (a.world > 1 && owner_of(nm, a.world) != a.rank) isremote = true;
+        else isnew = insert(a.table, a.cap, nm, full, a.tags, a.tag);
+    }
+    const unsigned rmask = __ballot_sync(FULL, isremote);
+    if (rmask) {                                  // owned by another rank: exchanged after the level
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.remote_cnt, (unsigned long long)__popc(rmask));
+        base = __shfl_sync(FULL, base, 0);
+        if (isremote) {
+            const unsigned long long pos = base + __popc(rmask & ((1u << lane) - 1));
+            if (pos < a.remote_cap) a.remote[pos] = nm;
+        }
     }
     const unsigned nmask = __ballot_sync(FULL, isnew);
     if (nmask) {
@@ -788,7 +814,62 @@ __global__ void k_collect(const M128 *tab, const uint8_t *tags, uint64_t cap, ui
     }
 }
 
+// received cells (owned here): insert with the level tag, new ones join the
+// next frontier (re-collected by tag if it overflows)
+__global__ void k_insert_recv(const M128 *list, uint64_t n, M128 *tab, uint8_t *tags, uint64_t cap, uint8_t tag,
+                              M128 *next, unsigned long long *next_cnt, uint64_t next_cap,
+                              unsigned long long *full_flag) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        bool full = false;
+        if (insert(tab, cap, list[i], full, tags, tag)) {
+            const unsigned long long pos = atomicAdd(next_cnt, 1ull);
+            if (pos < next_cap) next[pos] = list[i];
+        }
+        if (full) atomicAdd(full_flag, 1ull);
+    }
+}
+
+// counting sort of the remote cells by owner: counts, then scatter into
+// per-owner segments [off[o], off[o] + cnt[o])
+__global__ void k_owner_count(const M128 *list, uint64_t n, int world, unsigned long long *cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(cnt + owner_of(list[i], world), 1ull);
+}
+__global__ void k_owner_scatter(const M128 *list, uint64_t n, int world, unsigned long long *cursor, M128 *out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[atomicAdd(cursor + owner_of(list[i], world), 1ull)] = list[i];
+}
+
 }  // namespace walk
+
+int launch_insert_recv(const void *list, uint64_t n, void *tab, uint8_t *tags, uint64_t cap, uint8_t tag, void *next,
+                       unsigned long long *next_cnt, uint64_t next_cap, unsigned long long *full_flag, void *stream) {
+    if (n == 0) return 0;
+    const int grid = (int)std::min<uint64_t>((n + 255) / 256, 4096);
+    walk::k_insert_recv<<<grid, 256, 0, (cudaStream_t)stream>>>((const walk::M128 *)list, n, (walk::M128 *)tab, tags,
+                                                                cap, tag, (walk::M128 *)next, next_cnt, next_cap,
+                                                                full_flag);
+    launch_counter_add(1);
+    return (int)cudaGetLastError();
+}
+
+int launch_owner_count(const void *list, uint64_t n, int world, unsigned long long *cnt, void *stream) {
+    if (n == 0) return 0;
+    const int grid = (int)std::min<uint64_t>((n + 255) / 256, 4096);
+    walk::k_owner_count<<<grid, 256, 0, (cudaStream_t)stream>>>((const walk::M128 *)list, n, world, cnt);
+    launch_counter_add(1);
+    return (int)cudaGetLastError();
+}
+
+int launch_owner_scatter(const void *list, uint64_t n, int world, unsigned long long *cursor, void *out,
+                         void *stream) {
+    if (n == 0) return 0;
+    const int grid = (int)std::min<uint64_t>((n + 255) / 256, 4096);
+    walk::k_owner_scatter<<<grid, 256, 0, (cudaStream_t)stream>>>((const walk::M128 *)list, n, world, cursor,
+                                                                  (walk::M128 *)out);
+    launch_counter_add(1);
+    return (int)cudaGetLastError();
+}
 
 // host copy of the device hash of a 128-bit cell mask (for seeding the table)
 static uint64_t hmix(uint64_t z) {
@@ -883,8 +964,14 @@ int launch_walk(const int64_t *L, int K, int N, const void *cur, uint64_t ncur, 
                 unsigned long long *next_cnt, void *table, uint64_t cap, unsigned long long *counter,
                 unsigned long long *stats, int grid, void *stream, int64_t limV, int64_t limL,
                 unsigned long long *vol, int *fused, uint8_t *tags, unsigned tag, uint64_t next_cap,
-                int narrow, void *ovfl, unsigned long long *ovfl_cnt, uint64_t ovfl_cap, int vsafe) {
+                int narrow, void *ovfl, unsigned long long *ovfl_cnt, uint64_t ovfl_cap, int vsafe,
+                int world, int rank, void *remote, unsigned long long *remote_cnt, uint64_t remote_cap) {
     walk::WalkArgs a;
+    a.world = world;
+    a.rank = rank;
+    a.remote = (walk::M128 *)remote;
+    a.remote_cnt = remote_cnt;
+    a.remote_cap = remote_cap;
     a.narrow = narrow;
     a.vsafe = vsafe;
     a.ovfl = (walk::M128 *)ovfl;

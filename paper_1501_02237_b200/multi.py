@@ -89,3 +89,51 @@ def degree_distributed(plan: Plan, device, group=None, max_relift: int = 32) -> 
         return slots.cpu().tolist()
 
     return combine_with_relift(plan, partial, reduce, max_relift)
+
+
+class _CudaBuf:
+    """A raw device pointer seen by torch without a copy (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 2, "strides": None}
+
+
+def degree_walk_distributed(plan: Plan, group=None) -> Result:
+    """the cell walk with its hash set sharded over the ranks of
+    `group` (owner = hash(cell) mod world; one all-to-all of the neighbours
+    owned elsewhere per level; the volumes summed by one all-reduce).  NCCL:
+    the cells move device to device; gloo (tests): staged through the host."""
+    import torch
+    import torch.distributed as dist
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def allreduce_sum(vals):
+        t = torch.tensor(vals, dtype=torch.int64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return t.cpu().tolist()
+
+    def alltoall_counts(send):
+        t = torch.tensor(send, dtype=torch.int64, device=dev if backend == "nccl" else "cpu")
+        out = torch.empty_like(t)
+        dist.all_to_all_single(out, t, group=group)
+        return out.cpu().tolist()
+
+    def alltoall_cells(d_send, scnt, d_recv, rcnt):
+        ns, nr = 16 * sum(scnt), 16 * sum(rcnt)
+        send = torch.as_tensor(_CudaBuf(d_send, ns), device=dev) if ns else torch.empty(0, dtype=torch.uint8, device=dev)
+        recv = torch.as_tensor(_CudaBuf(d_recv, nr), device=dev) if nr else torch.empty(0, dtype=torch.uint8, device=dev)
+        if backend == "nccl":
+            dist.all_to_all_single(recv, send, output_split_sizes=[16 * c for c in rcnt],
+                                   input_split_sizes=[16 * c for c in scnt], group=group)
+            torch.cuda.current_stream().synchronize()
+        else:
+            hr = torch.empty(nr, dtype=torch.uint8)
+            dist.all_to_all_single(hr, send.cpu(), output_split_sizes=[16 * c for c in rcnt],
+                                   input_split_sizes=[16 * c for c in scnt], group=group)
+            if nr:
+                recv.copy_(hr)
+            torch.cuda.current_stream().synchronize()
+
+    return plan.degree_walk_sharded(allreduce_sum, alltoall_counts, alltoall_cells)

@@ -21,7 +21,7 @@
 constexpr int kIters = 4096;
 constexpr int kChains = 8;
 
-enum Op { IADD3, LOP3, IMAD, IMADW, MIX, SHF, ISETP };
+enum Op { IADD3, LOP3, IMAD, IMADW, MIX, SHF, ISETP, MIX_REUSE, MIX3, LOP3_REUSE };
 
 template <int OP>
 __global__ void __launch_bounds__(256) k_pipe(uint32_t *out, unsigned long long *cyc, uint32_t seed) {
@@ -52,6 +52,15 @@ __global__ void __launch_bounds__(256) k_pipe(uint32_t *out, unsigned long long 
                 else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(r[j]) : "r"(s[j]), "r"(s[(j + 3) & 7]));
             } else if constexpr (OP == SHF) {
                 asm volatile("shf.l.wrap.b32 %0, %0, %1, %2;" : "+r"(r[j]) : "r"(s[j]), "r"(s[(j + 3) & 7]));
+            } else if constexpr (OP == MIX_REUSE) {   // IMAD / LOP3 sharing two loop-invariant sources
+                if (j & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(r[j]) : "r"(s[0]), "r"(s[1]));
+                else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(r[j]) : "r"(s[0]), "r"(s[1]));
+            } else if constexpr (OP == MIX3) {        // IMAD : LOP3 : IADD3 = 3 : 3 : 2 (chain j mod 3)
+                if (j % 3 == 0) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(r[j]) : "r"(s[0]), "r"(s[1]));
+                else if (j % 3 == 1) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(r[j]) : "r"(s[0]), "r"(s[1]));
+                else asm volatile("{ .reg .u32 t; add.u32 t, %0, %1; add.u32 %0, t, %2; }" : "+r"(r[j]) : "r"(s[0]), "r"(s[1]));
+            } else if constexpr (OP == LOP3_REUSE) {
+                asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(r[j]) : "r"(s[0]), "r"(s[1]));
             } else {   // ISETP feeding a select (the facet tests' compare + select pattern)
                 asm volatile("{ .reg .pred p; setp.lt.s32 p, %0, %1; selp.u32 %0, %2, %0, p; }" : "+r"(r[j]) : "r"(s[j]), "r"(s[(j + 3) & 7]));
             }
@@ -109,7 +118,10 @@ int main() {
     run<SHF>("shf", "alu", 1.0, sms, bps, false);
     run<ISETP>("isetp_sel", "alu", 2.0, sms, bps, false);
     run<IMAD>("imad", "fma", 1.0, sms, bps, false);
-    run<MIX>("imad_lop3_mix", "alu+fma", 1.0, sms, bps, true);
+    run<MIX>("imad_lop3_mix", "alu+fma", 1.0, sms, bps, false);
+    run<MIX_REUSE>("imad_lop3_mix_reuse", "alu+fma", 1.0, sms, bps, false);
+    run<MIX3>("imad_lop3_iadd3_mix", "alu+fma", 1.0, sms, bps, false);
+    run<LOP3_REUSE>("lop3_reuse", "alu", 1.0, sms, bps, true);
     printf("}\n");
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
