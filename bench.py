@@ -222,13 +222,16 @@ def algorithmic_ops_per_candidate(K, nonsingular_frac, tested=2.0):
 
 def load_int_peak():
     """The measured integer issue peak (tools/intpipe_bench.cu on a B200):
-    lane-ops per SM clock, all integer pipes together and the ALU pipe alone."""
+    lane-ops per SM clock, the best integer instruction mix (ALU + FMA pipes
+    together) and the ALU pipe alone."""
     pth = os.path.join(ROOT, "profiles", "r2_intpipe_peaks.json")
     if os.path.exists(pth):
         d = json.load(open(pth))
-        alu = max(d[k]["lane_ops_per_clk_per_sm"] for k in ("iadd3", "lop3", "shf"))
-        allp = max(alu, d["imad"]["lane_ops_per_clk_per_sm"], d["imad_lop3_mix"]["lane_ops_per_clk_per_sm"])
-        return allp, alu, "measured (profiles/r2_intpipe_peaks.json)"
+        rows = {k: v for k, v in d.items() if isinstance(v, dict) and "lane_ops_per_clk_per_sm" in v}
+        alu = max(v["lane_ops_per_clk_per_sm"] for v in rows.values() if v["pipe"] == "alu")
+        allp = max(v["lane_ops_per_clk_per_sm"] for v in rows.values())
+        best = max(rows, key=lambda k: rows[k]["lane_ops_per_clk_per_sm"])
+        return allp, alu, f"measured, best mix '{best}' (profiles/r2_intpipe_peaks.json)"
     return 128.0, 64.0, "fallback: 4 SMSP x 32 lanes issue/clk/SM (not measured)"
 
 

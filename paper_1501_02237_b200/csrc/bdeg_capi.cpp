@@ -286,7 +286,7 @@ inline uint64_t colex_id(const std::vector<uint64_t> &B, const int *c, int d, in
 }
 
 int warps_per_sm_estimate(const bdeg_plan_s *p) {
-    const int ctas_lb = p->S >= 5 ? 3 : 4;               // __launch_bounds__ of k_enumerate
+    const int ctas_lb = 4;                               // __launch_bounds__ of k_enumerate
     const size_t smem = enumerate_smem_bytes(p->K, p->N, kernel_warps_per_cta());
     const int ctas_sm = (int)std::max<size_t>(1, (228 * 1024) / (smem + 1024));
     return std::min(ctas_lb, ctas_sm) * kernel_warps_per_cta();

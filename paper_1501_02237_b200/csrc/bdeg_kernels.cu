@@ -177,19 +177,6 @@ __device__ __forceinline__ float unford(uint32_t o) {   // inverse of ford
     return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
 }
 
-// bits [lo, hi) of a 64-bit point mask (0 <= lo <= hi <= 64)
-__device__ __forceinline__ uint64_t range_mask(int lo, int hi) {
-    const uint64_t h = hi >= 64 ? ~0ull : ((1ull << hi) - 1);
-    return lo >= 64 ? 0ull : (h & ~((1ull << lo) - 1));
-}
-// warp sum of a 64-bit value < 2^63 per lane (three exact 21-bit REDUX.SUMs)
-__device__ __forceinline__ uint64_t warp_sum63(uint64_t v) {
-    const uint32_t a = __reduce_add_sync(FULL, (uint32_t)(v & 0x1FFFFFu));
-    const uint32_t b = __reduce_add_sync(FULL, (uint32_t)((v >> 21) & 0x1FFFFFu));
-    const uint32_t c = __reduce_add_sync(FULL, (uint32_t)(v >> 42));
-    return (uint64_t)a + ((uint64_t)b << 21) + ((uint64_t)c << 42);
-}
-
 // Per-item accumulators (warp-uniform: every lane holds the same values).
 struct Acc {
     uint64_t vol_lo, vol_hi, singular, cand, updates;
@@ -449,30 +436,7 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
         acc.updates += 2ull * cx.N * nl;
         acc.cand += ((uint64_t)hi * (hi - 1) - (uint64_t)lo * (lo - 1)) / 2;   // sum of c
     }
-    // Leaf pivots c whose remaining V column is zero are dependent prefixes
-    // (every j < c singular): counted in bulk with one REDUX instead of one
-    // loop trip each (master space: most leaves).
-    uint64_t todo = range_mask(lo, hi);
-    if (!cx.partial && todo) {
-        uint64_t zmask = 0;
-#pragma unroll
-        for (int q = 0; q < NPL; ++q)
-            zmask |= (uint64_t)__ballot_sync(FULL, sv[q][0] == 0 && sv[q][1] == 0) << (32 * q);
-        const uint64_t dm = todo & zmask;
-        if (dm) {
-            uint32_t my = 0;
-#pragma unroll
-            for (int q = 0; q < NPL; ++q) {
-                const int l = cx.lane + 32 * q;
-                if ((dm >> l) & 1ull) my += (uint32_t)l;
-            }
-            acc.singular += __reduce_add_sync(FULL, my);
-            todo &= ~zmask;
-        }
-    }
-    while (todo) {
-        const int c = __ffsll((long long)todo) - 1;
-        todo &= todo - 1;
+    for (int c = lo; c < hi; ++c) {
         int jlo = 0, jhi = c;
         uint64_t nb = 0;
         if (cx.partial) {
@@ -614,35 +578,7 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
         bV = ((TIER == 0 || TIER == 3) ? (int64_t)INT32_MAX : cx.limV) * ap;
         bL = ((TIER == 0 || TIER == 3) ? (int64_t)INT32_MAX : cx.limL) * ap;
     }
-    // children c whose remaining V column is zero are dependent prefixes: their
-    // whole subtrees (C(c, i) candidates each) are singular, counted in bulk
-    uint64_t todo = range_mask(lo, hi);
-    if (!cx.partial && i < cx.fmin && todo) {
-        uint64_t zmask = 0;
-#pragma unroll
-        for (int q = 0; q < NPL; ++q) {
-            bool z = true;
-#pragma unroll
-            for (int r = 0; r < RV; ++r) z &= sv[q][r] == 0;
-            zmask |= (uint64_t)__ballot_sync(FULL, z) << (32 * q);
-        }
-        const uint64_t dm = todo & zmask;
-        if (dm) {
-            uint64_t my = 0;
-#pragma unroll
-            for (int q = 0; q < NPL; ++q) {
-                const int l = cx.lane + 32 * q;
-                if ((dm >> l) & 1ull) my += cx.C(l, i);
-            }
-            const uint64_t k = warp_sum63(my);
-            acc.singular += k;
-            acc.cand += k;
-            todo &= ~zmask;
-        }
-    }
-    while (todo) {
-        const int c = __ffsll((long long)todo) - 1;
-        todo &= todo - 1;
+    for (int c = lo; c < hi; ++c) {
         const uint64_t nb = base + cx.C(c, i + 1);
         const uint64_t ns = cx.C(c, i);
         if (cx.partial && cx.isect(nb, ns) == 0) continue;
@@ -913,10 +849,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 }
 
 template <int TIER, int NPL, int S>
-// Occupancy: deep register DFS (S >= 5) gets <= 168 registers (3 CTAs of 4
-// warps per SM), otherwise <= 128 (4 CTAs); measured best on B200.
+// Occupancy: <= 128 registers (4 CTAs of 4 warps per SM) at every DFS depth;
+// for S >= 5 this spills some of the deeper DFS state to local memory, which
+// measured faster than 168 registers at 3 CTAs (W_{2,6} 266.8 -> 254.5 ms,
+// tools/ab_bench.sh).
 #ifndef BDEG_MIN_BLOCKS
-#define BDEG_MIN_BLOCKS (S >= 5 ? 3 : 4)
+#define BDEG_MIN_BLOCKS 4
 #endif
 __global__ void __launch_bounds__(kWarps * 32, BDEG_MIN_BLOCKS)
 k_enumerate(const __grid_constant__ LaunchArgs a) {

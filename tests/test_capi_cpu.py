@@ -193,10 +193,14 @@ def test_planner_tier_follows_value_sizes():
     assert ei.value.status == B.bdeg.BDEG_E_TOO_LARGE and "Hadamard" in str(ei.value)
 
 
-def _warp_share(total, world, S, sms=148):
+def _warp_share(total, world, K, N, sms=148):
     # the planner's assumption on a host without a GPU: 148 SMs, resident
-    # warps from k_enumerate's launch bounds (4 CTAs x 4 warps, 3 CTAs for S >= 5)
-    return total / (world * sms * (12 if S >= 5 else 16))
+    # warps = 4 per CTA x min(4 CTAs (launch bounds), CTAs that fit in 228 KB
+    # of shared memory with k_enumerate's layout)
+    npl = 2 if N > 32 else 1
+    smem = ((K + 1) * N * 8 + 15) // 16 * 16 + 65 * 34 * 8 + 4 * 16 * 8 + 16 + 4 * (K + 1) * 32 * npl * 8
+    ctas = min(4, max(1, (228 * 1024) // (smem + 1024)))
+    return total / (world * sms * 4 * ctas)
 
 
 @pytest.mark.parametrize("name", ["c5", "w26", "w27"])
@@ -211,7 +215,7 @@ def test_work_queue_balance_at_world8(name):
     info = plan.info()
     total = math.comb(info.N, info.K)
     q = plan.queue_info()
-    share = _warp_share(total, 8, info.inner_levels)
+    share = _warp_share(total, 8, info.K, info.N)
     sizes = {}
     probe = {0, max(0, q["n_split"] - 1), q["n_split"], q["n_items"] - 1, q["n_static"] - 1}
     for pos in probe:
