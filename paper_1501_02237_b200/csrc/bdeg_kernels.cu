@@ -413,176 +413,6 @@ __device__ __forceinline__ bool node_dead(const typename Tr<TIER>::VV (&sv)[NPL]
     return __any_sync(FULL, below);
 }
 
-// Leaf level for 32 < N <= 48 points (two point slots per lane, the second
-// one only 1/2 to 1/4 used): two sibling leaves c, c+1 per pass over THREE
-// slot computations instead of four.  Slot 0 = points 0..31 for leaf c,
-// slot 1 = points 0..31 for leaf c+1, slot 2 = points 32..47 for leaf c on
-// lanes 0-15 and for leaf c+1 on lanes 16-31 (the parent's second slot is
-// replicated into the upper half-warp once per parent).  Each leaf's minima
-// are still one REDUX over the full warp (per-lane partials of its slots),
-// and the exact verification reads its own slots.  Same arithmetic and the
-// same tests as leaf_level (non-partial, non-dead leaves only).
-template <int TIER>
-__device__ __forceinline__ void leaf_level_pair(const typename Tr<TIER>::VV (&sv)[2][2],
-                                                const typename Tr<TIER>::VL (&sl)[2], int lo, int hi,
-                                                uint64_t inP, int64_t prev, const Ctx &cx, Acc &acc) {
-    typedef typename Tr<TIER>::VV VV;
-    typedef typename Tr<TIER>::VL VL;
-    const uint64_t gabs = (uint64_t)(prev < 0 ? -prev : prev);
-    const bool gneg = prev < 0;
-    const float INFF = __int_as_float(0x7f800000);
-    const int lane = cx.lane;
-    const int h = lane >> 4, l2 = lane & 15;
-    const int p2 = 32 + l2;                                   // slot-2 point of this lane
-    // the parent's second slot, replicated into the upper half-warp
-    const VV a2 = shfl<VV>(sv[1][0], l2), b2 = shfl<VV>(sv[1][1], l2);
-    const VL z2 = shfl<VL>(sl[1], l2);
-    const bool vp0 = lane < cx.N && !((inP >> lane) & 1ull);
-    const bool vp2 = p2 < cx.N && !((inP >> p2) & 1ull);
-    {
-        const uint64_t nl = (uint64_t)(hi - lo);
-        acc.leaves += (uint32_t)nl;
-        acc.updates += 2ull * cx.N * nl;
-        acc.cand += ((uint64_t)hi * (hi - 1) - (uint64_t)lo * (lo - 1)) / 2;   // sum of c
-    }
-    const uint32_t INF = 0xFF800000u;
-    for (int c = lo; c < hi; c += 2) {
-        // the two leaves' pivot columns
-        VV uu[2], vv[2];
-        VL zz[2];
-        bool act[2];
-#pragma unroll
-        for (int L = 0; L < 2; ++L) {
-            const int cl = c + L;
-            const int src = cl & 31;
-            const bool hs = (cl >> 5) != 0;
-            uu[L] = shfl<VV>(hs ? sv[1][0] : sv[0][0], src);
-            vv[L] = shfl<VV>(hs ? sv[1][1] : sv[0][1], src);
-            zz[L] = shfl<VL>(hs ? sl[1] : sl[0], src);
-            act[L] = cl < hi;
-            if (act[L] && uu[L] == 0 && vv[L] == 0) {         // dependent prefix: every j singular
-                acc.singular += (uint64_t)cl;
-                act[L] = false;
-            }
-        }
-        if (!act[0] && !act[1]) continue;
-        VV piv[2], ncs[2], pz[2];
-        VL ncz[2];
-        bool p0[2];
-#pragma unroll
-        for (int L = 0; L < 2; ++L) {
-            p0[L] = uu[L] != 0;
-            piv[L] = p0[L] ? uu[L] : vv[L];
-            ncs[L] = p0[L] ? -vv[L] : -uu[L];
-            const bool kneg = (piv[L] < 0) != gneg;
-            pz[L] = kneg ? (VV)-piv[L] : piv[L];
-            ncz[L] = kneg ? zz[L] : (VL)-zz[L];
-        }
-        // three slot computations
-        int64_t X[3], Y[3];
-        float fx[3], key[3];
-        bool val[3], cnt[3];
-#pragma unroll
-        for (int sl3 = 0; sl3 < 3; ++sl3) {
-            const int L = sl3 < 2 ? sl3 : h;
-            const int cl = c + L;
-            const bool pl = sl3 < 2 ? p0[sl3] : (h ? p0[1] : p0[0]);
-            const VV pv = sl3 < 2 ? piv[sl3] : (h ? piv[1] : piv[0]);
-            const VV nc = sl3 < 2 ? ncs[sl3] : (h ? ncs[1] : ncs[0]);
-            const VV pzz = sl3 < 2 ? pz[sl3] : (h ? pz[1] : pz[0]);
-            const VL nz = sl3 < 2 ? ncz[sl3] : (h ? ncz[1] : ncz[0]);
-            const VV ra = sl3 < 2 ? sv[0][0] : a2, rb = sl3 < 2 ? sv[0][1] : b2;
-            const VL rz = sl3 < 2 ? sl[0] : z2;
-            const int pt = sl3 < 2 ? lane : p2;
-            const VV prow = pl ? ra : rb;
-            const VV s = pl ? rb : ra;
-            X[sl3] = madw(pv, s, mulw(nc, prow));
-            if constexpr (TIER == 0 || TIER == 3) Y[sl3] = madw(pzz, rz, mulw(nz, prow));
-            else Y[sl3] = (int64_t)pzz * (int64_t)rz + (int64_t)nz * (int64_t)prow;
-            fx[sl3] = opaque((float)X[sl3]);
-            const bool actl = sl3 < 2 ? act[sl3] : (h ? act[1] : act[0]);
-            val[sl3] = actl && (sl3 < 2 ? vp0 : vp2) && pt != cl;
-            cnt[sl3] = actl && pt < cl;
-            key[sl3] = opaque((float)Y[sl3]) * rcp_approx(fx[sl3]);
-        }
-        // per-leaf partials: leaf L owns slot L and the slot-2 half h == L
-        float fp[2] = {INFF, INFF}, fm[2] = {INFF, INFF};
-        bool bad0[2] = {false, false};
-        unsigned sing[2] = {0, 0};
-#pragma unroll
-        for (int sl3 = 0; sl3 < 3; ++sl3) {
-            const bool zer = fx[sl3] == 0.0f;
-            const unsigned bz = __ballot_sync(FULL, cnt[sl3] && zer);
-            const float kp = (val[sl3] && fx[sl3] > 0.0f) ? key[sl3] : INFF;
-            const float km = (val[sl3] && fx[sl3] < 0.0f) ? -key[sl3] : INFF;
-            const bool b0 = val[sl3] && zer && Y[sl3] < 0;
-            if (sl3 < 2) {
-                sing[sl3] += __popc(bz);
-                fp[sl3] = fminf(fp[sl3], kp);
-                fm[sl3] = fminf(fm[sl3], km);
-                bad0[sl3] |= b0;
-            } else {
-                sing[0] += __popc(bz & 0xFFFFu);
-                sing[1] += __popc(bz >> 16);
-                fp[h] = fminf(fp[h], kp);
-                fm[h] = fminf(fm[h], km);
-                bad0[h] |= b0;
-            }
-        }
-        acc.singular += sing[0] + sing[1];
-        uint32_t mp[2], mm[2];
-#pragma unroll
-        for (int L = 0; L < 2; ++L) {
-            mp[L] = __reduce_min_sync(FULL, bad0[L] ? 0u : ford(fp[L]));
-            mm[L] = __reduce_min_sync(FULL, bad0[L] ? 0u : ford(fm[L]));
-        }
-#pragma unroll
-        for (int L = 0; L < 2; ++L) {
-            if (!act[L] || mp[L] == 0u || mm[L] == 0u) continue;
-            if (mp[L] != INF && mm[L] != INF && (~mm[L]) > mp[L] + 2 * kKeyMargin) continue;
-            const int cl = c + L;
-            const float tp = mp[L] == INF ? -INFF : unford(mp[L] + kKeyMargin);
-            const float tm = mm[L] == INF ? -INFF : unford(mm[L] + kKeyMargin);
-            // candidates: slot L (points 0..31) and slot 2 of half L (points 32..47)
-            const bool cdL = cnt[L] && ((fx[L] > 0.0f && key[L] <= tp) || (fx[L] < 0.0f && -key[L] <= tm));
-            const bool cd2 = h == L && cnt[2] && ((fx[2] > 0.0f && key[2] <= tp) || (fx[2] < 0.0f && -key[2] <= tm));
-            const unsigned b2 = __ballot_sync(FULL, cd2);
-            uint64_t candmask = (uint64_t)__ballot_sync(FULL, cdL) | ((uint64_t)((L ? b2 >> 16 : b2) & 0xFFFFu) << 32);
-            const int64_t XL = L ? X[1] : X[0], YL = L ? Y[1] : Y[0];
-            while (candmask) {                                 // exact verification (int128)
-                const int j = __ffsll((long long)candmask) - 1;
-                candmask &= candmask - 1;
-                const bool js = j >= 32;
-                const int srcl = js ? (j - 32) + 16 * L : j;
-                const int64_t xj = shfl<int64_t>(js ? X[2] : XL, srcl);
-                const int64_t yj = shfl<int64_t>(js ? Y[2] : YL, srcl);
-                bool bad = false, zero = false;
-                if (vp0 && lane != cl && lane != j) {
-                    i128 cr = (i128)xj * YL - (i128)XL * yj;
-                    if (xj < 0) cr = -cr;
-                    bad |= cr < 0;
-                    zero |= cr == 0;
-                }
-                if (h == L && vp2 && p2 != cl && p2 != j) {
-                    i128 cr = (i128)xj * Y[2] - (i128)X[2] * yj;
-                    if (xj < 0) cr = -cr;
-                    bad |= cr < 0;
-                    zero |= cr == 0;
-                }
-                if (__any_sync(FULL, bad)) continue;
-                if (__any_sync(FULL, zero)) {
-                    acc.ties += 1;                             // would-be cell on a tie (reading Z3)
-                } else {
-                    acc.cells += 1;
-                    const uint64_t vol = (uint64_t)(xj < 0 ? -xj : xj) / gabs;   // |det V_sigma|
-                    acc.add_vol(vol);
-                    cx.emit(inP | (1ull << cl) | (1ull << j), vol);
-                }
-            }
-        }
-    }
-}
-
 template <int TIER, int NPL>
 __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL][2],
                                            const typename Tr<TIER>::VL (&sl)[NPL], int lo, int hi,
@@ -590,14 +420,6 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
                                            Acc &acc, bool dead) {
     typedef typename Tr<TIER>::VV VV;
     typedef typename Tr<TIER>::VL VL;
-#ifndef BDEG_NO_PAIR_LEAF
-    if constexpr (NPL == 2) {
-        if (!cx.partial && !dead && cx.N <= 48 && hi > lo) {
-            leaf_level_pair<TIER>(sv, sl, lo, hi, inP, prev, cx, acc);
-            return;
-        }
-    }
-#endif
     const uint64_t gabs = (uint64_t)(prev < 0 ? -prev : prev);
     const bool gneg = prev < 0;
     const float INFF = __int_as_float(0x7f800000);
