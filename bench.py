@@ -384,6 +384,7 @@ def run_gpu(args):
             "data": "synthetic",
             "config": bench_config(wl, K, N, world),
             "kernel": {"inner_levels": info.inner_levels, "tier": info.tier, "work_items": plan.num_items(),
+                       "dead_subtrees_in_full_mode": info.dead_full,
                        "degree_only": bool(args.degree_only), "work_stealing_tail": steal},
             "time_to_degree_ms": e2e_step,
             "result": {"degree": res.degree, "cells": res.cells, "singular": res.singular,

@@ -111,6 +111,9 @@ typedef struct {
     uint64_t total_candidates; /* C(N,K)                                             */
     double plan_ms, kernel_ms, total_ms;
     uint64_t wide_reruns;    /* items re-run in the int128-value tier after leaving int64 */
+    int32_t dead_full;       /* 1: the planner sampled a degenerate configuration (>= 25 % singular
+                                K-subsets) and full mode detects cell-dead subtrees,
+                                whose leaves then only count singular candidates */
 } bdeg_result;
 
 #define BDEG_NSLOTS 16       /* int64 partial-result slots combined by one all-reduce(SUM) */

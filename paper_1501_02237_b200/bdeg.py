@@ -76,7 +76,8 @@ class _Result(ctypes.Structure):
                 ("seed_used", ctypes.c_uint64),
                 ("total_candidates", ctypes.c_uint64),
                 ("plan_ms", ctypes.c_double), ("kernel_ms", ctypes.c_double),
-                ("total_ms", ctypes.c_double), ("wide_reruns", ctypes.c_uint64)]
+                ("total_ms", ctypes.c_double), ("wide_reruns", ctypes.c_uint64),
+                ("dead_full", ctypes.c_int32)]
 
 
 _ALLREDUCE = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32)
@@ -242,6 +243,7 @@ class Result:
     kernel_ms: float
     total_ms: float
     wide_reruns: int = 0
+    dead_full: bool = False
     extra: dict = field(default_factory=dict)
 
 
@@ -257,7 +259,8 @@ def _result(r: _Result) -> Result:
                   consistent=bool(r.consistent), singular_complete=bool(r.singular_complete),
                   seed_used=r.seed_used,
                   total_candidates=r.total_candidates, plan_ms=r.plan_ms,
-                  kernel_ms=r.kernel_ms, total_ms=r.total_ms, wide_reruns=r.wide_reruns)
+                  kernel_ms=r.kernel_ms, total_ms=r.total_ms, wide_reruns=r.wide_reruns,
+                  dead_full=bool(r.dead_full))
 
 
 def _current_device():

@@ -11,12 +11,22 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <cstring>
 #include <string>
 #include <vector>
 
 using namespace bdeg;
+
+// The work queue of a plan (build_queue): a pure function of the plan's
+// shape (K, N, base depth, world, SMs, resident warps), so plans of one shape
+// share it (cached; the split table is uploaded once per device).
+struct WorkQueue {
+    std::vector<uint64_t> split;          // split items (depth << 58 | colex id), largest first
+    std::vector<uint64_t> grp_u, grp_cum; // grouped base-depth items
+    uint64_t nitems = 0, nstatic_steal = 0, grab = 1;
+};
 
 struct bdeg_plan_s {
     // inputs
@@ -36,13 +46,13 @@ struct bdeg_plan_s {
     int bits_v = 30, bits_l = 31;
     bool big = false;                 // N > 64: walk only (rank space beyond uint64 / lane slots)
     bool v_safe = false;              // every V-minor < 2^31 - 1 by Hadamard's bound (tier-0 kernels skip V checks)
+    bool dead_full = false;           // full mode: detect cell-dead subtrees (degenerate configurations)
     unsigned long long *steal = nullptr;   // cross-GPU item counters (2, by step parity), IPC-mapped
     int steal_parity = 0;
     uint64_t basis_lo = 0, basis_hi = 0;   // basis-seeded start cell (N > 64, generated lifting)
     uint64_t nblocks = 0, total = 0;      // base-depth items (colex range mode), C(N,K)
-    std::vector<uint64_t> split;          // work queue (build_queue): split items, then groups
-    std::vector<uint64_t> grp_u, grp_cum;
-    uint64_t nitems = 0, nstatic_steal = 0, grab = 1;
+    std::shared_ptr<const WorkQueue> q = std::make_shared<WorkQueue>();   // work queue (build_queue;
+                                                                          // shared by plans of one shape)
     uint64_t seed_used = 0;
     int relifts = 0;
     double plan_ms = 0;
@@ -96,7 +106,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 constexpr int kMaxGroups = 66;
 constexpr uint64_t kMaxOvfWords = 1ull << 21;   // base-depth item groups (one per smallest top index u)
 struct Layout {
-    size_t slots, ctr, L, B, q, split, gu, gc, total;
+    size_t slots, ctr, L, B, q, gu, gc, total;
 };
 Layout layout(const bdeg_plan_s *p) {
     Layout l;
@@ -106,7 +116,6 @@ Layout layout(const bdeg_plan_s *p) {
     l.L = off;     off = align256(off + (((size_t)(p->K + 1) * p->N * 8 + 15) & ~(size_t)15));
     l.B = off;     off = align256(off + (size_t)kBinomRows * kBinomCols * 8);
     l.q = off;     off = align256(off + 2 * p->ovf_words * 8);   // bitmaps A (narrow -> int64), B (-> int128)
-    l.split = off; off = align256(off + std::max<size_t>(1, p->split.size()) * 8);
     l.gu = off;    off = align256(off + kMaxGroups * 8);
     l.gc = off;    off = align256(off + kMaxGroups * 8);
     l.total = off;
@@ -292,57 +301,68 @@ int warps_per_sm_estimate(const bdeg_plan_s *p) {
     return std::min(ctas_lb, ctas_sm) * kernel_warps_per_cta();
 }
 
+std::mutex g_qmu;
+std::map<std::vector<int64_t>, std::shared_ptr<const WorkQueue>> g_queue_cache;
+
 void build_queue(bdeg_plan_s *p) {
     const int K = p->K, N = p->N, D = p->D;
     const auto &B = p->binom;
-    p->split.clear();
-    p->grp_u.clear();
-    p->grp_cum.clear();
     const int world = std::max(1, p->opt.world);
     const DevInfo &di = dev_info(p->opt.device);
     const double sms = di.ok ? di.sms : 148.0;
-    const double warps = sms * warps_per_sm_estimate(p);
+    const int wps = warps_per_sm_estimate(p);
+    const double warps = sms * wps;
     double frac = 0.25;                                   // largest item <= frac x a warp's share
     if (const char *e = std::getenv("BDEG_SPLIT_SHARE")) frac = std::atof(e);
     const bool do_split = (world > 1 || std::getenv("BDEG_SPLIT_1GPU")) && D > 0 && frac > 0;
     const double cap = std::max(1.0, (double)p->total / (world * warps) * frac);
-    std::vector<std::pair<uint64_t, uint64_t>> sp;        // (size, depth << 58 | id)
+    int64_t capbits;
+    std::memcpy(&capbits, &cap, 8);
+    const std::vector<int64_t> key{K, N, D, world, (int64_t)sms, wps, capbits, do_split ? 1 : 0};
+    {
+        std::lock_guard<std::mutex> lk(g_qmu);
+        auto it = g_queue_cache.find(key);
+        if (it != g_queue_cache.end()) { p->q = it->second; return; }
+    }
+    auto Q = std::make_shared<WorkQueue>();
+    // split items, bucketed by (depth, smallest index): every item of a bucket
+    // has the same size C(u, K-d), so ordering the buckets orders the items
+    std::map<std::pair<int, int>, std::vector<uint64_t>> buckets;
+    int c[kMaxK + 1];                                     // c[K-d .. K-1]: an item's top indices
+    // depth-first split of the node whose indices are c[K-d..K-1]
+    auto expand = [&](auto &&self, int d) -> void {
+        const int u = c[K - d];
+        const uint64_t size = C(B, u, K - d);
+        if ((double)size <= cap || d >= K - 1) {
+            buckets[{d, u}].push_back(((uint64_t)d << 58) | colex_id(B, c + (K - d), d, K - d));
+            return;
+        }
+        for (int u2 = K - d - 1; u2 < u; ++u2) {
+            c[K - d - 1] = u2;
+            self(self, d + 1);
+        }
+    };
     if (D == 0) {
-        p->grp_u.push_back(N);
-        p->grp_cum = {0, 1};
+        Q->grp_u.push_back(N);
+        Q->grp_cum = {0, 1};
     } else {
         uint64_t cum = 0;
         for (int u = N - D; u >= K - D; --u) {
             const uint64_t cnt = C(B, N - 1 - u, D - 1), sz = C(B, u, K - D);
             if (cnt == 0) continue;
             if (!do_split || (double)sz <= cap || D >= K - 1) {
-                p->grp_u.push_back(u);
-                p->grp_cum.push_back(cum);
+                Q->grp_u.push_back(u);
+                Q->grp_cum.push_back(cum);
                 cum += cnt;
                 continue;
             }
             // every item of the group: u, then a (D-1)-subset of {u+1..N-1} (colex successor)
-            std::vector<int> top(D);
+            int top[kMaxK];
             top[0] = u;
             for (int t = 1; t < D; ++t) top[t] = u + t;
             for (;;) {
-                // recursive split of the tuple (smallest first) down to size <= cap
-                std::vector<std::pair<std::vector<int>, int>> st{{top, D}};
-                while (!st.empty()) {
-                    auto [tp, d] = st.back();
-                    st.pop_back();
-                    const uint64_t size = C(B, tp[0], K - d);
-                    if ((double)size <= cap || d >= K - 1) {
-                        sp.push_back({size, ((uint64_t)d << 58) | colex_id(B, tp.data(), d, K - d)});
-                        continue;
-                    }
-                    for (int u2 = K - d - 1; u2 < tp[0]; ++u2) {
-                        std::vector<int> ch(d + 1);
-                        ch[0] = u2;
-                        std::copy(tp.begin(), tp.end(), ch.begin() + 1);
-                        st.push_back({ch, d + 1});
-                    }
-                }
+                for (int t = 0; t < D; ++t) c[K - D + t] = top[t];
+                expand(expand, D);
                 int t = 1;                                // next (D-1)-subset of {u+1..N-1}
                 while (t < D && (t + 1 < D ? top[t] + 1 >= top[t + 1] : top[t] + 1 >= N)) ++t;
                 if (t >= D) break;
@@ -350,28 +370,46 @@ void build_queue(bdeg_plan_s *p) {
                 for (int q = 1; q < t; ++q) top[q] = u + q;
             }
         }
-        p->grp_cum.push_back(cum);
+        Q->grp_cum.push_back(cum);
     }
-    std::stable_sort(sp.begin(), sp.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
-    p->split.resize(sp.size());
-    for (size_t i = 0; i < sp.size(); ++i) p->split[i] = sp[i].second;
-    p->nitems = p->split.size() + p->grp_cum.back();
+    std::vector<std::pair<uint64_t, const std::vector<uint64_t> *>> order;   // (size, bucket)
+    size_t nsplit = 0;
+    for (const auto &kv : buckets) {
+        order.push_back({C(B, kv.first.second, K - kv.first.first), &kv.second});
+        nsplit += kv.second.size();
+    }
+    std::stable_sort(order.begin(), order.end(), [](const auto &x, const auto &y) { return x.first > y.first; });
+    Q->split.clear();
+    Q->split.reserve(nsplit);
+    std::vector<uint64_t> split_size;                    // per split position (for the static share)
+    split_size.reserve(nsplit);
+    for (const auto &o : order) {
+        Q->split.insert(Q->split.end(), o.second->begin(), o.second->end());
+        split_size.insert(split_size.end(), o.second->size(), o.first);
+    }
+    Q->nitems = Q->split.size() + Q->grp_cum.back();
     // static share: the positions holding the first ~80% of the candidates
     // (balanced by the interleave); the rest is the stealing tail
     uint64_t acc = 0, pos = 0;
     const double want = 0.8 * (double)p->total;
-    for (size_t i = 0; i < sp.size() && acc < want; ++i, ++pos) acc += sp[i].first;
-    for (size_t g = 0; g + 1 < p->grp_cum.size() && acc < want; ++g) {
-        const uint64_t cnt = p->grp_cum[g + 1] - p->grp_cum[g];
-        const uint64_t sz = D == 0 ? p->total : C(B, p->grp_u[g], K - D);
+    for (size_t i = 0; i < split_size.size() && acc < want; ++i, ++pos) acc += split_size[i];
+    for (size_t g = 0; g + 1 < Q->grp_cum.size() && acc < want; ++g) {
+        const uint64_t cnt = Q->grp_cum[g + 1] - Q->grp_cum[g];
+        const uint64_t sz = D == 0 ? p->total : C(B, Q->grp_u[g], K - D);
         const uint64_t need = sz ? (uint64_t)std::ceil((want - (double)acc) / (double)sz) : cnt;
         const uint64_t take = std::min(cnt, need);
         acc += take * sz;
         pos += take;
     }
-    p->nstatic_steal = world > 1 ? std::min(pos, p->nitems) : p->nitems;
-    const uint64_t tail = p->nitems - p->nstatic_steal;
-    p->grab = std::max<uint64_t>(1, tail / (uint64_t)std::max(1.0, world * warps * 4));
+    Q->nstatic_steal = world > 1 ? std::min(pos, Q->nitems) : Q->nitems;
+    const uint64_t tail = Q->nitems - Q->nstatic_steal;
+    Q->grab = std::max<uint64_t>(1, tail / (uint64_t)std::max(1.0, world * warps * 4));
+    {
+        std::lock_guard<std::mutex> lk(g_qmu);
+        if (g_queue_cache.size() > 64) g_queue_cache.clear();   // plans keep their own reference
+        g_queue_cache[key] = Q;
+    }
+    p->q = Q;
 }
 
 // queue position -> (depth, tuple of the largest indices, smallest first)
@@ -379,9 +417,9 @@ void decode_position(const bdeg_plan_s *p, uint64_t pos, int &d, std::vector<int
     const auto &B = p->binom;
     const int K = p->K;
     top.clear();
-    if (pos < p->split.size()) {
-        d = (int)(p->split[pos] >> 58);
-        uint64_t r = p->split[pos] & ((1ull << 58) - 1);
+    if (pos < p->q->split.size()) {
+        d = (int)(p->q->split[pos] >> 58);
+        uint64_t r = p->q->split[pos] & ((1ull << 58) - 1);
         top.assign(d, 0);
         for (int t = d - 1; t >= 0; --t) {
             int x = t;
@@ -393,11 +431,11 @@ void decode_position(const bdeg_plan_s *p, uint64_t pos, int &d, std::vector<int
     }
     d = p->D;
     if (d == 0) return;
-    const uint64_t q = pos - p->split.size();
+    const uint64_t q = pos - p->q->split.size();
     size_t g = 0;
-    while (g + 2 < p->grp_cum.size() && p->grp_cum[g + 1] <= q) ++g;
-    const int u = p->grp_u[g];
-    uint64_t r = q - p->grp_cum[g];
+    while (g + 2 < p->q->grp_cum.size() && p->q->grp_cum[g + 1] <= q) ++g;
+    const int u = p->q->grp_u[g];
+    uint64_t r = q - p->q->grp_cum[g];
     top.assign(d, 0);
     top[0] = u;
     for (int t = d - 2; t >= 0; --t) {
@@ -406,6 +444,47 @@ void decode_position(const bdeg_plan_s *p, uint64_t pos, int &d, std::vector<int
         r -= C(B, x, t + 1);
         top[t + 1] = x + u + 1;
     }
+}
+
+// Fraction of singular K-subsets among `samples` random ones (det mod the
+// prime 2^31 - 1; a det divisible by p counts as singular: a heuristic).
+// Degenerate configurations (master spaces: 60-93 % singular) have many
+// cell-dead subtrees, which full mode then detects; random
+// configurations (C5: 0.04 %) skip the per-node test.
+double sampled_singular_fraction(const bdeg_plan_s *p, int samples) {
+    const int K = p->K, N = p->N;
+    const uint64_t P = 2147483647ull;                     // Mersenne: x mod P by shifts
+    auto red = [P](uint64_t x) { x = (x & P) + (x >> 31); x = (x & P) + (x >> 31); return x >= P ? x - P : x; };
+    SplitMix64 g(0xdeadull ^ p->seed_used);
+    std::vector<int> idx(N);
+    std::vector<uint64_t> M((size_t)K * K);
+    int sing = 0;
+    for (int s = 0; s < samples; ++s) {
+        for (int i = 0; i < N; ++i) idx[i] = i;
+        for (int i = 0; i < K; ++i) std::swap(idx[i], idx[i + (int)(g.next() % (uint64_t)(N - i))]);
+        for (int r = 0; r < K; ++r)
+            for (int c = 0; c < K; ++c) {
+                int64_t v = p->V[(size_t)idx[c] * K + r] % (int64_t)P;
+                M[(size_t)r * K + c] = (uint64_t)(v < 0 ? v + (int64_t)P : v);
+            }
+        bool zero = false;
+        for (int c = 0; c < K && !zero; ++c) {
+            int pr = -1;
+            for (int r = c; r < K; ++r) if (M[(size_t)r * K + c]) { pr = r; break; }
+            if (pr < 0) { zero = true; break; }
+            if (pr != c) for (int t = 0; t < K; ++t) std::swap(M[(size_t)pr * K + t], M[(size_t)c * K + t]);
+            // division-free step (row_r <- piv row_r - f row_c): the rank is all that matters
+            const uint64_t piv = M[(size_t)c * K + c];
+            for (int r = c + 1; r < K; ++r) {
+                const uint64_t f = M[(size_t)r * K + c];
+                if (!f) continue;
+                for (int t = c; t < K; ++t)
+                    M[(size_t)r * K + t] = red(red(piv * M[(size_t)r * K + t]) + P - red(f * M[(size_t)c * K + t]));
+            }
+        }
+        sing += zero;
+    }
+    return samples ? (double)sing / samples : 0.0;
 }
 
 void choose_tier_and_blocks(bdeg_plan_s *p) {
@@ -442,6 +521,8 @@ void choose_tier_and_blocks(bdeg_plan_s *p) {
     if (p->opt.flags & BDEG_FLAG_FORCE_TIER1) p->tier = 1;
     if (p->opt.flags & BDEG_FLAG_FORCE_TIER2) p->tier = 2;
     raw_tier_bounds(p);
+    if (const char *e = std::getenv("BDEG_DEAD_FULL")) p->dead_full = std::atoi(e) != 0;   // A/B knob
+    else p->dead_full = sampled_singular_fraction(p, 32) > 0.25;
     // Register-DFS depth S (deep: the DFS does one fraction-free step per
     // tree node), smem prefix T = K-1-S, and the work-item depth D >= T chosen
     // so that the largest item C(N-D, K-D) is a small fraction of the
@@ -580,7 +661,7 @@ bdeg_status finish_plan(bdeg_plan_s *p) {
     // the re-run bitmaps have one bit per work item (either mode), up to 2^27
     // items (16 MB each); positions beyond that are counted in SLOT_QFULL and
     // the synchronous entry points redo the whole space in tier 2
-    p->ovf_words = std::min<uint64_t>((std::max<uint64_t>(std::max(p->nblocks, p->nitems), 1) + 63) / 64,
+    p->ovf_words = std::min<uint64_t>((std::max<uint64_t>(std::max(p->nblocks, p->q->nitems), 1) + 63) / 64,
                                       kMaxOvfWords);
     p->l_dirty = true;
     return BDEG_OK;
@@ -590,6 +671,26 @@ bdeg_status finish_plan(bdeg_plan_s *p) {
 void rebuild_points(bdeg_plan_s *p) {
     build_points(p->fe, p->lift.data(), !(p->opt.flags & BDEG_FLAG_NO_HOMOG_SHORTCUT), p->K, p->N, p->V,
                  p->w, p->point_of_var, p->origin_index);
+}
+
+// The split-item table of a work queue on the plan's device: uploaded once
+// per (device, queue) and kept for the process (queues are cached by shape).
+std::map<std::pair<int, const WorkQueue *>, std::pair<std::shared_ptr<const WorkQueue>, uint64_t *>> g_dsplit;
+
+uint64_t *device_split_table(bdeg_plan_s *p) {
+    if (p->q->split.empty()) return nullptr;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const auto key = std::make_pair(p->opt.device, p->q.get());
+    auto it = g_dsplit.find(key);
+    if (it != g_dsplit.end()) return it->second.second;
+    uint64_t *d = nullptr;
+    if (cudaMalloc(&d, p->q->split.size() * 8) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, p->q->split.data(), p->q->split.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return nullptr;
+    }
+    g_dsplit[key] = {p->q, d};                 // holds the queue: the pointer key stays unique
+    return d;
 }
 
 void *pool_get(int d, size_t bytes, size_t *got) {
@@ -654,7 +755,7 @@ bdeg_status ensure_device(bdeg_plan_s *p) {
         p->d_ovfq = reinterpret_cast<unsigned long long *>(p->ws + L.q);
         if ((e = cudaMemsetAsync(p->d_ovfq, 0, 2 * p->ovf_words * 8, (cudaStream_t)p->opt.stream)) != cudaSuccess)
             return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));      // the replay keeps it clean after this
-        p->d_split = reinterpret_cast<uint64_t *>(p->ws + L.split);
+        p->d_split = device_split_table(p);
         p->d_gu = reinterpret_cast<uint64_t *>(p->ws + L.gu);
         p->d_gc = reinterpret_cast<uint64_t *>(p->ws + L.gc);
         cudaStream_t st = (cudaStream_t)p->opt.stream;
@@ -662,14 +763,11 @@ bdeg_status ensure_device(bdeg_plan_s *p) {
             cudaSuccess)
             return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
         // the work queue (plan-constant): split items and the group tables
-        if (!p->split.empty() &&
-            (e = cudaMemcpyAsync(p->d_split, p->split.data(), p->split.size() * 8, cudaMemcpyHostToDevice, st)) !=
-                cudaSuccess)
-            return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
-        if (!p->grp_u.empty() &&
-            ((e = cudaMemcpyAsync(p->d_gu, p->grp_u.data(), p->grp_u.size() * 8, cudaMemcpyHostToDevice, st)) !=
+        if (!p->q->split.empty() && !p->d_split) return fail(p, BDEG_E_CUDA, "upload of the split-item table failed");
+        if (!p->q->grp_u.empty() &&
+            ((e = cudaMemcpyAsync(p->d_gu, p->q->grp_u.data(), p->q->grp_u.size() * 8, cudaMemcpyHostToDevice, st)) !=
                  cudaSuccess ||
-             (e = cudaMemcpyAsync(p->d_gc, p->grp_cum.data(), p->grp_cum.size() * 8, cudaMemcpyHostToDevice, st)) !=
+             (e = cudaMemcpyAsync(p->d_gc, p->q->grp_cum.data(), p->q->grp_cum.size() * 8, cudaMemcpyHostToDevice, st)) !=
                  cudaSuccess))
             return fail(p, BDEG_E_CUDA, cudaGetErrorString(e));
         if ((e = cudaEventCreate(&p->ev0)) != cudaSuccess || (e = cudaEventCreate(&p->ev1)) != cudaSuccess)
@@ -723,11 +821,11 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     if (b == 0 && e >= p->total) {        // the whole space: the largest-first work queue
         a.mode = 1;
         a.split = p->d_split;
-        a.n_split = p->split.size();
+        a.n_split = p->q->split.size();
         a.grp_u = p->d_gu;
         a.grp_cum = p->d_gc;
-        a.n_grp = (int)p->grp_u.size();
-        a.n_items = p->nitems;
+        a.n_grp = (int)p->q->grp_u.size();
+        a.n_items = p->q->nitems;
     } else {                              // a rank range: contiguous base-depth items
         a.mode = 0;
         a.blk_first = block_of(p, b);
@@ -745,6 +843,7 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     if (a.tier == 0 && p->v_safe) a.tier = 3;   // tier 0 without V-row range checks (Hadamard)
     a.bits_v = p->bits_v;
     a.degree_only = (p->opt.flags & BDEG_FLAG_DEGREE_ONLY) ? 1 : 0;
+    a.dead_full = p->dead_full ? 1 : 0;
     a.cells_out = cells_out;
     a.cells_cnt = cells_cnt;
     a.cells_cap = cells_cap;
@@ -758,8 +857,8 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
     if (p->steal && world > 1 && a.mode == 1) {
         // static interleaved share of the first ~80% of the candidates, then
         // one global tail queue over all GPUs (system-scope atomics, NVLink)
-        a.n_static = p->nstatic_steal;
-        a.grab = p->grab;
+        a.n_static = p->q->nstatic_steal;
+        a.grab = p->q->grab;
         a.gcounter = p->steal + p->steal_parity;
         a.system_counter = 1;
         if (rank == 0) a.reset_next = p->steal + (p->steal_parity ^ 1);
@@ -809,6 +908,7 @@ void fill_front(const bdeg_plan_s *p, bdeg_result *r) {
     r->consistent = p->points_mode ? 1 : p->fe.consistent;
     r->seed_used = p->seed_used;
     r->singular_complete = (p->opt.flags & BDEG_FLAG_DEGREE_ONLY) ? 0 : 1;
+    r->dead_full = p->dead_full ? 1 : 0;
     r->relifts = p->relifts;
     r->total_candidates = p->total;
     r->plan_ms = p->plan_ms;
@@ -1690,11 +1790,11 @@ bdeg_status bdeg_finalize(bdeg_plan_t p, const int64_t *h_slots, bdeg_result *ou
     return BDEG_OK;
 }
 
-uint64_t bdeg_num_items(bdeg_plan_t p) { return (p && p->K > 0) ? p->nitems : 0; }
+uint64_t bdeg_num_items(bdeg_plan_t p) { return (p && p->K > 0) ? p->q->nitems : 0; }
 
 bdeg_status bdeg_item_range(bdeg_plan_t p, uint64_t item, uint64_t *begin, uint64_t *end) {
     if (!p || !begin || !end) return fail(p, BDEG_E_INVALID, "NULL argument");
-    if (p->K == 0 || p->big || item >= p->nitems) return fail(p, BDEG_E_INVALID, "item out of range");
+    if (p->K == 0 || p->big || item >= p->q->nitems) return fail(p, BDEG_E_INVALID, "item out of range");
     int d = 0;
     std::vector<int> top;
     decode_position(p, item, d, top);
@@ -1710,10 +1810,10 @@ bdeg_status bdeg_queue_info(bdeg_plan_t p, uint64_t *n_items, uint64_t *n_split,
                             uint64_t *grab) {
     if (!p) return fail(p, BDEG_E_INVALID, "NULL plan");
     const bool k = p->K > 0 && !p->big;
-    if (n_items) *n_items = k ? p->nitems : 0;
-    if (n_split) *n_split = k ? p->split.size() : 0;
-    if (n_static) *n_static = k ? p->nstatic_steal : 0;
-    if (grab) *grab = k ? p->grab : 0;
+    if (n_items) *n_items = k ? p->q->nitems : 0;
+    if (n_split) *n_split = k ? p->q->split.size() : 0;
+    if (n_static) *n_static = k ? p->q->nstatic_steal : 0;
+    if (grab) *grab = k ? p->q->grab : 0;
     return BDEG_OK;
 }
 

@@ -96,6 +96,7 @@ struct LaunchArgs {
     const unsigned long long *replay_gate;   // replays: the slot counting the marked items (0 => exit at once)
     int grid, block;                  // launch shape
     int degree_only;                  // skip cell-dead subtrees
+    int dead_full;                    // full mode: detect cell-dead subtrees, their leaves count singular only
     unsigned long long *cells_out;    // optional (mask, |det|) output of the cells found
     unsigned long long *cells_cnt;
     uint64_t cells_cap;

@@ -211,6 +211,7 @@ struct Ctx {
     int mytop;           // this lane's entry of the item tuple: c_{kd + lane} (lane < D)
     uint64_t irb, ire;   // the item's candidates n [rank_begin, rank_end)
     bool deg_only;       // skip cell-dead subtrees (singular count becomes a lower bound)
+    bool dead_full;      // full mode: find cell-dead subtrees too (their leaves count singular only)
     bool partial;        // the item is cut by the rank range
     __device__ __forceinline__ uint64_t C(int n, int k) const { return B[n * kBinomCols + k]; }
     // |[base, base+size) n [irb, ire)| (subtrees below the item level lie inside the item)
@@ -620,7 +621,10 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
             // loops are index-bounded, so garbage values cannot hang the warp
             elim_step<TIER, NPL, RV>(sv, sl, cv, cl, pr, piv, dv, bV, bL, cx, ov, ol, ovf);
             const uint64_t cinP = inP | (1ull << c);
-            const bool cdead = cx.deg_only && (dead || node_dead<TIER, NPL, RV - 1>(ov, ol, cinP, (int64_t)piv, cx));
+            // cell-dead subtree: degree-only skips it; full mode keeps
+            // walking it for the singular count but its leaves skip the facet test
+            const bool cdead = dead || (cx.dead_full || cx.deg_only) &&
+                                           node_dead<TIER, NPL, RV - 1>(ov, ol, cinP, (int64_t)piv, cx);
             if (cdead && cx.deg_only) {          // no cell in the subtree: skip it
                 acc.cand += (i >= cx.fmin) ? cx.ire - cx.irb : cx.isect(nb, ns);
                 continue;
@@ -834,7 +838,7 @@ __device__ void process_item(int D, int mytop, const int64_t *Lsm, int64_t *scr,
         for (int q = 0; q < NPL; ++q) { xx[q] = (int64_t)sv[q][0]; yy[q] = (int64_t)sl[q]; }
         leaf_test<NPL>(xx, yy, ctop, ttop, inP, prev > 0 ? 1 : -1, 1, cx, acc);
     } else {
-        const bool dead = cx.deg_only && node_dead<TIER, NPL, S + 1>(sv, sl, inP, prev, cx);
+        const bool dead = (cx.dead_full || cx.deg_only) && node_dead<TIER, NPL, S + 1>(sv, sl, inP, prev, cx);
         if (dead && cx.deg_only) {
             acc.cand += cx.ire - cx.irb;
             return;
@@ -917,6 +921,7 @@ k_enumerate(const __grid_constant__ LaunchArgs a) {
 
     cx.D = a.P.D;
     cx.deg_only = a.degree_only != 0;
+    cx.dead_full = a.dead_full != 0;
     cx.kd = K - a.P.D;
     cx.fmin = S + 1;
     cx.mytop = 0;
@@ -1141,6 +1146,7 @@ k_enumerate_wide(const __grid_constant__ LaunchArgs a) {
     cx.fmin = 0;
     cx.mytop = 0;
     cx.deg_only = false;
+    cx.dead_full = false;
     uint64_t vol_lo = 0, vol_hi = 0, cells = 0, singular = 0, cand = 0, ties = 0, items = 0, fatal = 0;
     unsigned long long rbits = 0, rword = 0;
     for (;;) {
