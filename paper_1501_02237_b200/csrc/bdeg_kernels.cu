@@ -483,8 +483,9 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
         float fp = INFF, fm = INFF;
         bool bad0 = false;
         unsigned sing = 0;
-#pragma unroll
-        for (int q = 0; q < NPL; ++q) {
+        const uint32_t INF = 0xFF800000u;                  // ford(+inf): group empty
+        // slot q's points: X, Y, the slope key and this lane's partial minima
+        auto eval = [&](const int q) {
             const int l = cx.lane + 32 * q;
             const VV prow = p0 ? sv[q][0] : sv[q][1];
             const VV s = p0 ? sv[q][1] : sv[q][0];
@@ -501,13 +502,34 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
             key[q] = fy * rcp_approx(fx[q]);       // slope, |error| << kKeyMargin units
             fp = fminf(fp, (val && fx[q] > 0.0f) ? key[q] : INFF);
             fm = fminf(fm, (val && fx[q] < 0.0f) ? -key[q] : INFF);
+        };
+        eval(0);
+        if constexpr (NPL == 2) {
+            // Early rejection on points 0..31 alone: a violation among a subset of
+            // the points is one of the whole set (its min over x > 0 can only
+            // drop, its max over x < 0 only rise).  Most leaves hold no cell, so
+            // slot 1 (32 < N <= 64) is evaluated only for the few that survive;
+            // the singular count still needs slot 1's X when c > 32.
+            const uint32_t mp0 = __reduce_min_sync(FULL, bad0 ? 0u : ford(fp));
+            const uint32_t mm0 = __reduce_min_sync(FULL, bad0 ? 0u : ford(fm));
+            if (mp0 == 0u || mm0 == 0u || (mp0 != INF && mm0 != INF && (~mm0) > mp0 + 2 * kKeyMargin)) {
+                if (jhi > 32) {
+                    const VV prow = p0 ? sv[NPL - 1][0] : sv[NPL - 1][1];
+                    const VV s = p0 ? sv[NPL - 1][1] : sv[NPL - 1][0];
+                    const int64_t x1 = madw(piv, s, mulw(ncs, prow));
+                    const int l = cx.lane + 32;
+                    sing += __popc(__ballot_sync(FULL, l >= jlo && l < jhi && x1 == 0));
+                }
+                acc.singular += sing;
+                continue;
+            }
+            eval(NPL - 1);
         }
         acc.singular += sing;
         // a point of span(P) strictly below rejects the leaf: force key 0 (no real key is 0)
         const uint32_t mp = __reduce_min_sync(FULL, bad0 ? 0u : ford(fp));   // ~ min slope, x > 0
         const uint32_t mm = __reduce_min_sync(FULL, bad0 ? 0u : ford(fm));   // ~ -max slope, x < 0
         if (mp == 0u || mm == 0u) continue;
-        const uint32_t INF = 0xFF800000u;                  // ford(+inf): group empty
         // both cells need  max_{x<0} slope < min_{x>0} slope; ford(-x) = ~ford(x)
         if (mp != INF && mm != INF && (~mm) > mp + 2 * kKeyMargin) continue;
         const float tp = mp == INF ? -INFF : unford(mp + kKeyMargin);
