@@ -4,6 +4,7 @@
 #include "bdeg_internal.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for nsys / ncu --nvtx
 
 #include <algorithm>
 #include <chrono>
@@ -74,6 +75,12 @@ struct bdeg_plan_s {
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range for the scope (plan / enumerate / replays / walk level / finalize)
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
 
 double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -804,6 +811,7 @@ bdeg_status enqueue_range(bdeg_plan_s *p, uint64_t b, uint64_t e, unsigned long 
                           int world, int force_tier, unsigned long long *cells_out = nullptr,
                           unsigned long long *cells_cnt = nullptr, uint64_t cells_cap = 0,
                           bool first_cell_search = false) {
+    Nvtx range("bdeg enumerate (main + replays)");
     cudaStream_t st = (cudaStream_t)p->opt.stream;
     cudaError_t ce;
     if ((ce = cudaMemsetAsync(slots, 0, kNSlots * 8, st)) != cudaSuccess) return fail(p, BDEG_E_CUDA, cudaGetErrorString(ce));
@@ -1010,6 +1018,7 @@ uint64_t pow2_at_least(uint64_t x) {
 // One breadth-first walk of the subdivision.  Cell masks are
 // 16-byte {lo, hi} pairs.
 bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
+    Nvtx range("bdeg walk");
     cudaStream_t st = (cudaStream_t)p->opt.stream;
     const double t0 = now_ms();
     uint64_t start[2] = {0, 0};
@@ -1304,6 +1313,7 @@ bdeg_status walk_once(bdeg_plan_s *p, bdeg_result *r, double *kms) {
 // decisions (termination, ties, overflow) through one small all-reduce, and
 // the volumes summed by the owners.  Same kernels as walk_once.
 bdeg_status walk_sharded(bdeg_plan_s *p, const bdeg_comm *cm, bdeg_result *r, double *kms) {
+    Nvtx range("bdeg sharded walk");
     cudaStream_t st = (cudaStream_t)p->opt.stream;
     const double t0 = now_ms();
     const int W = std::max(1, p->opt.world), R = p->opt.rank;
@@ -1575,6 +1585,7 @@ void bdeg_default_options(bdeg_options *o) {
 }
 
 bdeg_status bdeg_plan(const bdeg_problem *prob, const bdeg_options *opt, bdeg_plan_t *out) {
+    Nvtx range("bdeg plan (front end + planner)");
     if (!prob || !out) return fail(nullptr, BDEG_E_INVALID, "NULL argument");
     if (prob->n < 1 || prob->m < 0 || (prob->m > 0 && !prob->A))
         return fail(nullptr, BDEG_E_INVALID, "bad problem shape");
@@ -1625,6 +1636,7 @@ bdeg_status bdeg_plan(const bdeg_problem *prob, const bdeg_options *opt, bdeg_pl
 
 bdeg_status bdeg_plan_points(int32_t K, int32_t N, const int64_t *V, const int64_t *lifting,
                              const bdeg_options *opt, bdeg_plan_t *out) {
+    Nvtx range("bdeg plan (points)");
     if (!V || !out || K < 1 || N < K) return fail(nullptr, BDEG_E_INVALID, "bad point configuration");
     const double t0 = now_ms();
     bdeg_plan_s *p = new bdeg_plan_s();
@@ -1765,6 +1777,7 @@ bdeg_status bdeg_degree_partial(bdeg_plan_t p, int64_t *d_slots) {
 }
 
 bdeg_status bdeg_finalize(bdeg_plan_t p, const int64_t *h_slots, bdeg_result *out) {
+    Nvtx range("bdeg finalize");
     if (!p || !h_slots || !out) return fail(p, BDEG_E_INVALID, "NULL argument");
     bdeg_result r;
     fill_front(p, &r);
@@ -2005,6 +2018,7 @@ bdeg_status bdeg_dimension_modp(int32_t n, int32_t m, const int64_t *A, int32_t 
 
 bdeg_status bdeg_smith_gpu(int32_t n, int32_t m, const int64_t *A, int32_t device, void *stream, int64_t *rank,
                            uint64_t *comp_lo, uint64_t *comp_hi, int64_t *unit_pivots) {
+    Nvtx range("bdeg smith (unit pivots)");
     if (!A || !rank || n < 1 || m < 0) return fail(nullptr, BDEG_E_INVALID, "bad arguments");
     for (size_t i = 0; i < (size_t)n * m; ++i)
         if (A[i] >= ((int64_t)1 << 61) || A[i] <= -((int64_t)1 << 61))

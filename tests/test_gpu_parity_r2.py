@@ -238,3 +238,19 @@ def test_exact_smith_matches_oracle_snf():
         rank, comps, _ = B.smith_gpu(A)
         r = analyze(A, b)
         assert (len(A) - rank, comps) == (r["dim"], r["components"])
+
+
+def test_checkpoint_resume(tmp_path):
+    # a long enumeration survives a restart — the ledger of finished
+    # rank intervals and the exact running sums resume to the full result
+    from paper_1501_02237_b200.checkpoint import degree_checkpointed
+    V, w = W.c5_points(3, n_points=30, dim=6)
+    full = B.Plan.from_points(V, w).degree()
+    path = str(tmp_path / "ledger.json")
+    part = degree_checkpointed(B.Plan.from_points(V, w), path, chunks=7, stop_after=3)
+    assert part["candidates"] < full.candidates
+    done = degree_checkpointed(B.Plan.from_points(V, w), path, chunks=7)      # a fresh process would do this
+    assert (done["degree"], done["cells"], done["singular"], done["candidates"]) == \
+        (full.degree, full.cells, full.singular, full.candidates)
+    with pytest.raises(B.BdegError):                                          # another lifting: refused
+        degree_checkpointed(B.Plan.from_points(V, [x + 1 for x in w]), path, chunks=7)
