@@ -123,7 +123,9 @@ void bdeg_default_options(bdeg_options *o);
 
 /* Front end + planner (CPU) for x^A = b.  Copies the inputs.  Returns
  * BDEG_E_INCONSISTENT for an empty solution set, BDEG_E_TOO_LARGE when the
- * point configuration exceeds N <= 64, K <= 32, BDEG_E_INVALID on bad
+ * point configuration exceeds N <= 128, K <= 32 (N > 64: the walk only), a
+ * coordinate or lifting reaches 2^62, or Hadamard's bound on the lifted
+ * minors reaches 2^125 (beyond the int128 tier), BDEG_E_INVALID on bad
  * shapes.  d = 0 plans are valid (degree 1, no device work). */
 bdeg_status bdeg_plan(const bdeg_problem *prob, const bdeg_options *opt, bdeg_plan_t *out);
 
@@ -247,14 +249,15 @@ typedef struct {
 bdeg_status bdeg_degree_walk_sharded(bdeg_plan_t plan, const bdeg_comm *comm, bdeg_result *out);
 
 /* Cross-GPU dynamic work stealing.  One process (rank 0)
- * creates a pair of item counters in its GPU's memory and exports them as a
+ * creates a pair of tail counters in its GPU's memory and exports them as a
  * CUDA IPC handle (BDEG_STEAL_HANDLE_BYTES bytes); every rank (rank 0 included,
  * via the same handle in another process, or its own) attaches them to its
- * plan.  bdeg_degree_partial then takes work items from ONE global
- * largest-first queue with system-scope atomics over NVLink instead of the
- * static interleaved shard; the counters alternate by step parity and rank 0's
- * launch zeroes the idle one, so all ranks must call bdeg_degree_partial once
- * per step, separated by the result all-reduce (which orders the steps). */
+ * plan.  bdeg_degree_partial then takes its static interleaved share of the
+ * queue's first n_static positions (bdeg_queue_info) and the remaining
+ * positions from the ONE global counter, `grab` per system-scope atomic over
+ * NVLink; the counters alternate by step parity and rank 0's launch zeroes
+ * the idle one, so all ranks must call bdeg_degree_partial once per step,
+ * separated by the result all-reduce (which orders the steps). */
 #define BDEG_STEAL_HANDLE_BYTES 64
 bdeg_status bdeg_steal_create(int32_t device, uint8_t *out_handle);
 bdeg_status bdeg_steal_attach(bdeg_plan_t plan, const uint8_t *handle);
