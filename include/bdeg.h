@@ -82,7 +82,7 @@ typedef struct {
     int32_t rank, world;     /* this process's shard of rank space (default 0, 1)    */
     void *stream;            /* cudaStream_t for every launch/copy; NULL = default   */
     uint32_t flags;          /* BDEG_FLAG_*                                          */
-    int32_t inner_levels;    /* register-resident DFS depth S in 0..6; -1 = auto     */
+    int32_t inner_levels;    /* register-resident DFS depth S in 0..7; -1 = auto     */
     int32_t ctas_per_sm;     /* persistent CTAs per SM; 0 = auto                     */
 } bdeg_options;
 

@@ -12,7 +12,7 @@ typedef unsigned __int128 u128;
 
 constexpr int kMaxN = 64;    // points: the kernel maps one point to a lane slot (2 slots/lane)
 constexpr int kMaxK = 32;    // subset size (K+1 rows of the lifted matrix, <= 33)
-constexpr int kMaxInner = 6;   // register-resident DFS levels (template parameter S)
+constexpr int kMaxInner = 7;   // register-resident DFS levels (template parameter S)
 constexpr int kBinomRows = 65;
 constexpr int kBinomCols = 34;
 

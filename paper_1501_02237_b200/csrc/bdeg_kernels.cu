@@ -1327,7 +1327,7 @@ static KernFn pick(int tier, int npl, int S) {
 #define BDEG_K(T_, P_, S_) \
     if (tier == T_ && npl == P_ && S == S_) return dev::k_enumerate<T_, P_, S_>;
 #define BDEG_KS(T_, P_) BDEG_K(T_, P_, 0) BDEG_K(T_, P_, 1) BDEG_K(T_, P_, 2) BDEG_K(T_, P_, 3) \
-    BDEG_K(T_, P_, 4) BDEG_K(T_, P_, 5) BDEG_K(T_, P_, 6)
+    BDEG_K(T_, P_, 4) BDEG_K(T_, P_, 5) BDEG_K(T_, P_, 6) BDEG_K(T_, P_, 7)
     BDEG_KS(0, 1) BDEG_KS(0, 2) BDEG_KS(1, 1) BDEG_KS(1, 2) BDEG_KS(2, 1) BDEG_KS(2, 2)
     BDEG_KS(3, 1) BDEG_KS(3, 2)
 #undef BDEG_KS
