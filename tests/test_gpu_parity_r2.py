@@ -2,7 +2,7 @@
 
   * the cell walk with N > 64 points (basis-seeded lifting, 3-4 point slots
     per lane) against the C oracle under the lifting the plan actually uses;
-  * arithmetic tiers 1 and 2 with deep register DFS (S = 4..6, K = 10..14)
+  * arithmetic tiers 1 and 2 with deep register DFS (S = 4..7, K = 10..14)
     on 20-40-bit values, sampled rank intervals against the C oracle;
   * a re-lift that really happens (the oracle shows ties at attempt 0);
   * the full C5 bench configuration against SURVEY §8.d.1's pins;
@@ -68,7 +68,7 @@ def _sample_ranges(total, n, span, seed):
     return out
 
 
-@pytest.mark.parametrize("S", [4, 5, 6])
+@pytest.mark.parametrize("S", [4, 5, 6, 7])
 @pytest.mark.parametrize("tierflag,box,lift_bits", [(0x8, 2, 16), (0x8, 2, 24), (0x20, 4, 20), (0x20, 4, 28)])
 def test_deep_dfs_tiers_on_wide_values(S, tierflag, box, lift_bits):
     # K = 10..14 with a register DFS of depth S (T = K-1-S prefix levels in
