@@ -41,3 +41,26 @@ def test_gpu_arm_line():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= d["steps"]
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+def test_gpu_arm_two_ranks_line():
+    # the driver's N > 1 launch (torchrun, one rank per GPU); on a 1-GPU box the
+    # two ranks share the GPU over gloo (BDEG_SHARE_GPU=1).  Rank 0 prints ONE
+    # line; the combined result is cross-checked against a single-GPU run inside.
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, BDEG_SHARE_GPU="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--steps", "3", "--warmup", "3"], cwd=ROOT, env=env,
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["result"]["degree"] == 51983602 and d["result"]["candidates"] == 76904685
+    assert d["kernel"]["work_stealing_tail"] is True and d["cpu_baseline"] is None
