@@ -425,7 +425,7 @@ def main():
                     help="candidates per oracle sample (cpu_baseline / reference arm)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--degree-only", action="store_true",
-                    help="skip cell-dead subtrees (singular becomes a lower bound)")
+                    help="skip cell-dead subtrees (singular becomes an upper bound)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

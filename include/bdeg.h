@@ -71,8 +71,8 @@ typedef struct {
 #define BDEG_FLAG_NO_RELIFT         0x10u /* report BDEG_E_DEGENERATE instead of re-lifting       */
 #define BDEG_FLAG_DEGREE_ONLY       0x40u /* skip cell-dead subtrees (a point of the prefix span
                                              lies strictly below: no cell); degree,
-                                             cells, candidates stay exact, singular becomes a
-                                             lower bound (singular_complete = 0)              */
+                                             cells, candidates stay exact, singular becomes an
+                                             upper bound (singular_complete = 0)              */
 
 typedef struct {
     uint64_t seed;           /* seed of the generated lifting (and of re-lifts)      */

@@ -496,6 +496,13 @@ double sampled_singular_fraction(const bdeg_plan_s *p, int samples) {
 
 void choose_tier_and_blocks(bdeg_plan_s *p) {
     p->total = C(p->binom, p->N, p->K);
+    // Register-DFS depth S (deep: the DFS does one fraction-free step per
+    // tree node) and smem prefix T = K-1-S
+    const int smax = std::min(kMaxInner, p->K - 1);
+    // measured (tools/sweep_libs.sh): S = 3 for K = 8, 4-5 for K = 12, 6 for K >= 14
+    const int sauto = std::min(smax, std::max(3, p->K / 2 - 1));
+    p->S = p->opt.inner_levels >= 0 ? std::min(p->opt.inner_levels, smax) : sauto;
+    p->T = p->K - 1 - p->S;
     int bv = 0, bl = 0;
     sample_bits(p, bv, bl);
     p->bits_v = std::min(30, std::max(bv + 2, 8));
@@ -530,15 +537,9 @@ void choose_tier_and_blocks(bdeg_plan_s *p) {
     raw_tier_bounds(p);
     if (const char *e = std::getenv("BDEG_DEAD_FULL")) p->dead_full = std::atoi(e) != 0;   // A/B knob
     else p->dead_full = sampled_singular_fraction(p, 32) > 0.25;
-    // Register-DFS depth S (deep: the DFS does one fraction-free step per
-    // tree node), smem prefix T = K-1-S, and the work-item depth D >= T chosen
+    // The work-item depth D >= T chosen
     // so that the largest item C(N-D, K-D) is a small fraction of the
     // per-warp share (items are processed largest-first).
-    const int smax = std::min(kMaxInner, p->K - 1);
-    // measured (tools/sweep_libs.sh): S = 3 for K = 8, 4-5 for K = 12, 6 for K >= 14
-    const int sauto = std::min(smax, std::max(3, p->K / 2 - 1));
-    p->S = p->opt.inner_levels >= 0 ? std::min(p->opt.inner_levels, smax) : sauto;
-    p->T = p->K - 1 - p->S;
     const double warps = 148.0 * 16.0;
     double factor = 0.25;
     if (const char *e = std::getenv("BDEG_ITEM_FACTOR")) factor = std::atof(e);   // tuning knob

@@ -176,10 +176,13 @@ __device__ __forceinline__ float unford(uint32_t o) {   // inverse of ford
 }
 
 // Per-item accumulators (warp-uniform: every lane holds the same values).
+// The item counts its NON-singular candidates (nonsing); its singular count is
+// then |item| - nonsing, so dependent subtrees (no pivot: every candidate
+// below singular) cost nothing at all -- no subtree-size bookkeeping.
 struct Acc {
-    uint64_t vol_lo, vol_hi, singular, cand, updates;
+    uint64_t vol_lo, vol_hi, nonsing, cand, updates;
     uint32_t cells, ties, leaves, dead;
-    __device__ void zero() { vol_lo = vol_hi = singular = cand = updates = 0; cells = ties = leaves = dead = 0; }
+    __device__ void zero() { vol_lo = vol_hi = nonsing = cand = updates = 0; cells = ties = leaves = dead = 0; }
     __device__ void add_vol(uint64_t v) {
         uint64_t t = vol_lo + v;
         vol_hi += (t < vol_lo);
@@ -194,7 +197,7 @@ struct WAcc {
         uint64_t t = vol_lo + o.vol_lo;
         vol_hi += (t < vol_lo) + o.vol_hi;
         vol_lo = t;
-        cells += o.cells; singular += o.singular; cand += o.cand; ties += o.ties;
+        cells += o.cells; singular += o.cand - o.nonsing; cand += o.cand; ties += o.ties;
         updates += o.updates; leaves += o.leaves; dead += o.dead;
     }
 };
@@ -208,7 +211,7 @@ struct Ctx {
     int D, kd, fmin;     // item depth, K - D, smallest forced DFS level
     int mytop;           // this lane's entry of the item tuple: c_{kd + lane} (lane < D)
     uint64_t irb, ire;   // the item's candidates n [rank_begin, rank_end)
-    bool deg_only;       // skip cell-dead subtrees (singular count becomes a lower bound)
+    bool deg_only;       // skip cell-dead subtrees (singular count becomes an upper bound)
     bool dead_full;      // full mode: find cell-dead subtrees too (their leaves count singular only)
     bool partial;        // the item is cut by the rank range
     __device__ __forceinline__ uint64_t C(int n, int k) const { return B[n * kBinomCols + k]; }
@@ -252,7 +255,6 @@ __device__ __forceinline__ void leaf_test(const int64_t (&x)[NPL], const int64_t
         if (cx.ire < base + (uint64_t)c1) jhi = (cx.ire <= base) ? 0 : (int)(cx.ire - base);
         if (jlo >= jhi) return;
     }
-    acc.cand += (uint64_t)(jhi - jlo);
     acc.leaves += 1;
     // warp-uniform point masks: countable j in [jlo, jhi); valid l = not in P, < N
     const uint64_t cntm = ((jhi >= 64) ? ~0ull : ((1ull << jhi) - 1)) & ~((1ull << jlo) - 1);
@@ -269,7 +271,7 @@ __device__ __forceinline__ void leaf_test(const int64_t (&x)[NPL], const int64_t
         const bool v = (vq & lanebit) != 0;
         yk[q] = kappa > 0 ? y[q] : -y[q];
         const bool zx = x[q] == 0;
-        sing += __popc(__ballot_sync(FULL, zx) & (uint32_t)(cntm >> (32 * q)));
+        sing += __popc(__ballot_sync(FULL, !zx) & (uint32_t)(cntm >> (32 * q)));   // non-singular
         bad0 |= v && zx && yk[q] < 0;
         // slope key yk/x (approximate; error << kKeyMargin key units)
         const uint32_t o = ford(__fdividef((float)yk[q], (float)x[q]));
@@ -277,7 +279,7 @@ __device__ __forceinline__ void leaf_test(const int64_t (&x)[NPL], const int64_t
         if (v && x[q] > 0) kp = min(kp, o);
         if (v && x[q] < 0) km = min(km, ~o);
     }
-    acc.singular += sing;
+    acc.nonsing += sing;
     if (__any_sync(FULL, bad0)) return;          // a point of span(P) lies strictly below
     const uint32_t mp = __reduce_min_sync(FULL, kp);   // ~ min slope over x > 0
     const uint32_t mm = __reduce_min_sync(FULL, km);   // ~ max slope over x < 0 (complemented)
@@ -451,21 +453,39 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
     typedef typename Tr<TIER>::VL VL;
     const bool gneg = prev < 0;
     const float INFF = __int_as_float(0x7f800000);
-    if (!R && hi > lo) {                       // whole leaves: counters per parent
+    if (hi <= lo) return;
+    if (!R) {                                  // whole leaves: counters per parent
         const uint64_t nl = (uint64_t)(hi - lo);
         acc.leaves += (uint32_t)nl;
         acc.updates += 2ull * cx.N * nl;
-        acc.cand += ((uint64_t)hi * (hi - 1) - (uint64_t)lo * (lo - 1)) / 2;   // sum of c
     }
+    // X of this lane's slot-q point for the leaf with pivot column (uc, vc)
+    auto xval = [&](const VV uc, const VV nvc, const int q) -> int64_t {
+        return madw(uc, sv[q][1], mulw(nvc, sv[q][0]));
+    };
+    // rejected: a point strictly below (-> -inf) or min_{X>0} k + min_{X<0} k < 0
+    // beyond the key error
+    auto rejected = [&](const float mp, const float mm) {
+        return mp == -INFF || (mp + mm < -(fabsf(mp) + fabsf(mm)) * kRelMargin);
+    };
+    // Y of a point (e = the pivot row's entry, z = lift) for the leaf's (pz, ncz)
+    auto yval = [&](const VV pz, const VL ncz, const VV el, const VL zl) -> int64_t {
+        if constexpr (TIER == 0 || TIER == 3) return madw(pz, zl, mulw(ncz, el));
+        else return (int64_t)pz * (int64_t)zl + (int64_t)ncz * (int64_t)el;
+    };
+    struct Ev {
+        int64_t X, Y;
+        float fx, key;
+    };
+    // One leaf c, held in slot SC (compile time: the loop below is split at 32).
     auto leaf = [&](auto SCC, const int c) {
-        constexpr int SC = decltype(SCC)::value;   // slot holding point c
+        constexpr int SC = decltype(SCC)::value;
         int jlo = 0, jhi = c;
         if constexpr (R) {
             const uint64_t nb = base + (uint64_t)c * (uint64_t)(c - 1) / 2;   // + C(c, 2)
             if (cx.irb > nb) jlo = (cx.irb - nb >= (uint64_t)c) ? c : (int)(cx.irb - nb);
             if (cx.ire < nb + (uint64_t)c) jhi = (cx.ire <= nb) ? 0 : (int)(cx.ire - nb);
             if (jlo >= jhi) return;
-            acc.cand += (uint64_t)(jhi - jlo);
             acc.leaves += 1;
             acc.updates += 2ull * cx.N;
         }
@@ -473,22 +493,19 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
         const VV uc = shfl<VV>(sv[SC][0], src);
         const VV vc = shfl<VV>(sv[SC][1], src);
         const VL zc = shfl<VL>(sl[SC], src);
-        if ((uc | vc) == 0) {                      // dependent prefix: every j singular
-            acc.singular += (uint64_t)(jhi - jlo);
-            return;
-        }
+        if ((uc | vc) == 0) return;                // dependent prefix: every j singular
         // countable j per slot (uniform masks)
         const uint32_t m0 = R ? bits_range(jlo, jhi < 32 ? jhi : 32) : (SC == 0 ? bits_range(0, c) : 0xFFFFFFFFu);
         const uint32_t m1 = (NPL > 1 && SC == 1)
                                 ? (R ? bits_range(jlo > 32 ? jlo - 32 : 0, jhi > 32 ? jhi - 32 : 0)
                                      : bits_range(0, c - 32))
                                 : 0u;
+        const uint32_t n0 = m0, n1 = m1;
         const VV nvc = -vc;
-        auto xval = [&](const int q) -> int64_t { return madw(uc, sv[q][1], mulw(nvc, sv[q][0])); };
-        if (dead) {                                // no cell below: singular count only
-            unsigned sd = __popc(__ballot_sync(FULL, xval(0) == 0) & m0);
-            if constexpr (NPL > 1 && SC == 1) sd += __popc(__ballot_sync(FULL, xval(1) == 0) & m1);
-            acc.singular += sd;
+        if (dead) {                                // no cell below: non-singular count only
+            unsigned sd = __popc(__ballot_sync(FULL, xval(uc, nvc, 0) != 0) & n0);
+            if constexpr (NPL > 1 && SC == 1) sd += __popc(__ballot_sync(FULL, xval(uc, nvc, 1) != 0) & n1);
+            acc.nonsing += sd;
             acc.dead += 1;
             return;
         }
@@ -497,46 +514,39 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
         const bool kneg = (ec < 0) != gneg;
         const VV pz = kneg ? (VV)-ec : ec;
         const VL ncz = kneg ? zc : (VL)-zc;
-        int64_t X[NPL], Y[NPL];
-        float fx[NPL], key[NPL];
+        Ev ev[NPL];
         float fp = INFF, fm = INFF;
         bool bad0 = false;
-        unsigned sing = 0;
-        auto eval = [&](const int q, const uint32_t m) {
-            X[q] = xval(q);
-            const VV el = p0 ? sv[q][0] : sv[q][1];
-            if constexpr (TIER == 0 || TIER == 3) Y[q] = madw(pz, sl[q], mulw(ncz, el));
-            else Y[q] = (int64_t)pz * (int64_t)sl[q] + (int64_t)ncz * (int64_t)el;
-            fx[q] = opaque((float)X[q]);
-            const float fy = opaque((float)Y[q]);
-            const bool zer = fx[q] == 0.0f;
-            sing += __popc(__ballot_sync(FULL, zer) & m);
+        unsigned nons = 0;
+        auto eval = [&](const int q) {
+            ev[q].X = xval(uc, nvc, q);
+            ev[q].Y = yval(pz, ncz, p0 ? sv[q][0] : sv[q][1], sl[q]);
+            ev[q].fx = opaque((float)ev[q].X);
+            const float fy = opaque((float)ev[q].Y);
+            const bool zer = ev[q].fx == 0.0f;
             bad0 |= zer && fy < 0.0f;
-            key[q] = fy * rcp_approx(fabsf(fx[q]));
-            fp = fminf(fp, fx[q] > 0.0f ? key[q] : INFF);
-            fm = fminf(fm, fx[q] < 0.0f ? key[q] : INFF);
+            ev[q].key = fy * rcp_approx(fabsf(ev[q].fx));
+            fp = fminf(fp, ev[q].fx > 0.0f ? ev[q].key : INFF);
+            fm = fminf(fm, ev[q].fx < 0.0f ? ev[q].key : INFF);
         };
-        // rejected: a point strictly below (bad0 -> -inf) or
-        // min_{X>0} k + min_{X<0} k < 0 beyond the key error
-        auto rejected = [&](const float mp, const float mm) {
-            return mp == -INFF || (mp + mm < -(fabsf(mp) + fabsf(mm)) * kRelMargin);
-        };
-        eval(0, m0);
+        eval(0);
+        nons += __popc(__ballot_sync(FULL, ev[0].fx != 0.0f) & n0);
         if constexpr (NPL == 2) {
             // Early rejection on points 0..31 alone: a violation among a subset of
             // the points is one of the whole set (its min over X > 0 can only
             // drop, its max over X < 0 only rise); slot 1 is evaluated for the
-            // few leaves that survive, and for the singular count when c > 32.
+            // few leaves that survive, and for the count when c > 32.
             const float mp0 = redux_min_f32(bad0 ? -INFF : fp);
             const float mm0 = redux_min_f32(fm);
             if (rejected(mp0, mm0)) {
-                if constexpr (SC == 1) sing += __popc(__ballot_sync(FULL, xval(1) == 0) & m1);
-                acc.singular += sing;
+                if constexpr (SC == 1) nons += __popc(__ballot_sync(FULL, xval(uc, nvc, 1) != 0) & n1);
+                acc.nonsing += nons;
                 return;
             }
-            eval(1, m1);
+            eval(1);
+            nons += __popc(__ballot_sync(FULL, ev[1].fx != 0.0f) & n1);
         }
-        acc.singular += sing;
+        acc.nonsing += nons;
         const float mp = redux_min_f32(bad0 ? -INFF : fp);
         const float mm = redux_min_f32(fm);
         if (rejected(mp, mm)) return;
@@ -545,7 +555,7 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
         uint64_t candmask = 0;
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
-            const bool cd = (fx[q] > 0.0f && key[q] <= tp) || (fx[q] < 0.0f && key[q] <= tm);
+            const bool cd = (ev[q].fx > 0.0f && ev[q].key <= tp) || (ev[q].fx < 0.0f && ev[q].key <= tm);
             candmask |= (uint64_t)(__ballot_sync(FULL, cd) & (q == 0 ? m0 : m1)) << (32 * q);
         }
         const uint64_t gabs = (uint64_t)(prev < 0 ? -prev : prev);
@@ -554,14 +564,14 @@ __device__ __forceinline__ void leaf_level(const typename Tr<TIER>::VV (&sv)[NPL
             candmask &= candmask - 1;
             const int jl = j & 31;
             const bool js = NPL > 1 && (j >> 5) != 0;
-            const int64_t xj = shfl<int64_t>(js ? X[NPL - 1] : X[0], jl);
-            const int64_t yj = shfl<int64_t>(js ? Y[NPL - 1] : Y[0], jl);
+            const int64_t xj = shfl<int64_t>(js ? ev[NPL - 1].X : ev[0].X, jl);
+            const int64_t yj = shfl<int64_t>(js ? ev[NPL - 1].Y : ev[0].Y, jl);
             bool bad = false, zero = false;
 #pragma unroll
             for (int q = 0; q < NPL; ++q) {
                 const int l = cx.lane + 32 * q;
                 if (l < cx.N && !((inP >> l) & 1ull) && l != c && l != j) {
-                    i128 cr = (i128)xj * Y[q] - (i128)X[q] * yj;
+                    i128 cr = (i128)xj * ev[q].Y - (i128)ev[q].X * yj;
                     if (xj < 0) cr = -cr;
                     bad |= cr < 0;
                     zero |= cr == 0;
@@ -625,12 +635,7 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
         int pr = -1;
 #pragma unroll
         for (int r = RV - 1; r >= 0; --r) if (cv[r] != 0) pr = r;
-        if (pr < 0) {                        // prefix dependent: whole subtree singular
-            const uint64_t k = (i >= cx.fmin) ? cx.ire - cx.irb : (R ? cx.isect(nb, cx.C(c, i)) : cx.C(c, i));
-            acc.singular += k;
-            acc.cand += k;
-            continue;
-        }
+        if (pr < 0) continue;                // prefix dependent: whole subtree singular
         VV piv = cv[0];
 #pragma unroll
         for (int r = 1; r < RV; ++r) if (pr == r) piv = cv[r];
@@ -661,10 +666,7 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
             // walking it for the singular count but its leaves skip the facet test
             const bool cdead = dead || (cx.dead_full || cx.deg_only) &&
                                            node_dead<TIER, NPL, RV - 1>(ov, ol, cinP, (int64_t)piv, cx);
-            if (cdead && cx.deg_only) {          // no cell in the subtree: skip it
-                acc.cand += (i >= cx.fmin) ? cx.ire - cx.irb : (R ? cx.isect(nb, cx.C(c, i)) : cx.C(c, i));
-                continue;
-            }
+            if (cdead && cx.deg_only) continue;  // no cell in the subtree: skip it
             inner_dfs<TIER, NPL, RV - 1, R>(ov, ol, c, nb, cinP, (int64_t)piv, cx, acc, ovf, cdead);
         }
     }
@@ -755,6 +757,7 @@ __device__ void process_item(int D, int mytop, const int64_t *Lsm, int64_t *scr,
         cx.irb = lo;
         cx.ire = hi;
         cx.partial = (lo != tall) || (hi != tall + isize);
+        acc.cand = hi - lo;                   // the item's candidates: a contiguous colex interval
     }
     uint64_t inP = 0;
     {
@@ -779,12 +782,7 @@ __device__ void process_item(int D, int mytop, const int64_t *Lsm, int64_t *scr,
             const int p = __shfl_sync(FULL, mytop, D - 1 - t);   // pivot order c_{K-1}, c_{K-2}, ...
             const bool nz = (lane < K) && ((alive >> lane) & 1ull) && scr[lane * NP + p] != 0;
             const unsigned bal = __ballot_sync(FULL, nz);
-            if (bal == 0) {                                       // dependent prefix
-                const uint64_t k = cx.isect(tall, isize);
-                acc.singular += k;
-                acc.cand += k;
-                return;
-            }
+            if (bal == 0) return;                                 // dependent prefix: all singular
             const int r = __ffs(bal) - 1;
             const int64_t piv = scr[r * NP + p];
             const Div dv = make_div(prev);
@@ -880,10 +878,7 @@ __device__ void process_item(int D, int mytop, const int64_t *Lsm, int64_t *scr,
         leaf_test<NPL>(xx, yy, ctop, ttop, inP, prev > 0 ? 1 : -1, 1, cx, acc);
     } else {
         const bool dead = (cx.dead_full || cx.deg_only) && node_dead<TIER, NPL, S + 1>(sv, sl, inP, prev, cx);
-        if (dead && cx.deg_only) {
-            acc.cand += cx.ire - cx.irb;
-            return;
-        }
+        if (dead && cx.deg_only) return;
         inner_dfs<TIER, NPL, S + 1, R>(sv, sl, ctop, ttop, inP, prev, cx, acc, ovf, dead);
     }
 }
