@@ -1,0 +1,5 @@
+#!/bin/bash
+# round 2, call Z5: interleaved two-leaf pass (ILP) -- GPU parity suite, then A/B against 44f04bc
+cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q -x -k "not twins" > gpurun_out/r2z5_gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r2z5_gpu_tests.log; tail -3 gpurun_out/r2z5_gpu_tests.log
+timeout 1200 bash tools/ab_bench.sh r2z5_ilp scratch/libbdeg_44f04bc.so -
