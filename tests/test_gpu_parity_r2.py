@@ -254,3 +254,30 @@ def test_checkpoint_resume(tmp_path):
         (full.degree, full.cells, full.singular, full.candidates)
     with pytest.raises(B.BdegError):                                          # another lifting: refused
         degree_checkpointed(B.Plan.from_points(V, [x + 1 for x in w]), path, chunks=7)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_nearly_affine_lifting(seed):
+    # Heights w_l = 2^22 (lam . v_l) + 2^30 + r_l with r_l < 2^10: the affine part
+    # leaves the regular subdivision unchanged (it is decided by r alone) but
+    # inflates every lift minor to ~2^50, so each facet value is a small exact
+    # difference of huge terms -- the wide-lift tier path, the leaf's fp32 keys
+    # and their relative margins on values far from the C5 ones.
+    # C5-shaped points (N = 40: both point slots), K = 6; bit-exact vs the C oracle.
+    rng = random.Random(seed)
+    pts = set()
+    while len(pts) < 40:
+        pts.add(tuple(rng.randint(-3, 3) for _ in range(5)))
+    V = [(1,) + p for p in sorted(pts)]
+    lam = [rng.randint(-5, 5) for _ in range(6)]
+    w = [(1 << 22) * sum(a * b for a, b in zip(lam, v)) + (1 << 30) + rng.randrange(1 << 10) for v in V]
+    K, N = 6, len(V)
+    o = enumerate_range(K, V, w, threads=8)
+    if o["ties"]:
+        pytest.skip("degenerate lifting drawn")
+    r = B.Plan.from_points(V, w).degree_range(0, math.comb(N, K))
+    for k in ("volume", "cells", "singular", "candidates", "ties"):
+        assert {"volume": r.degree, "cells": r.cells, "singular": r.singular, "candidates": r.candidates,
+                "ties": r.ties}[k] == o[k], (k, seed)
+    full = B.Plan.from_points(V, w).degree()          # the whole-space (work-queue) kernels
+    assert (full.degree, full.cells, full.singular) == (r.degree, r.cells, r.singular)
