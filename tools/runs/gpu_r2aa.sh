@@ -9,4 +9,4 @@ timeout 600 python bench.py --workload w26 --steps 3 --warmup 3 --no-cpu-baselin
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2aa_launches_c5.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_enumerate -s 12 -c 1 -o gpurun_out/r2aa_prof_c5 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_enumerate -s 12 -c 1 -o gpurun_out/r2aa_prof_w26 python bench.py --workload w26 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-timeout 900 bash tools/gpu_r2p.sh > /dev/null 2>&1; cp gpurun_out/r2p_table3_enum.jsonl gpurun_out/r2aa_table3_enum.jsonl; cut -c1-250 gpurun_out/r2aa_table3_enum.jsonl
+timeout 900 bash tools/runs/gpu_r2p.sh > /dev/null 2>&1; cp gpurun_out/r2p_table3_enum.jsonl gpurun_out/r2aa_table3_enum.jsonl; cut -c1-250 gpurun_out/r2aa_table3_enum.jsonl

@@ -1,5 +1,5 @@
 #!/bin/bash
-# round 2, call AH: parent certificates with the batched count-only leaves -- GPU suite, A/B vs 44f04bc,
+# round 2, call AI: parent certificates with the batched count-only leaves -- GPU suite, A/B vs 44f04bc,
 # dead-leaf counts
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/r2ai_gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r2ai_gpu_tests.log; tail -3 gpurun_out/r2ai_gpu_tests.log

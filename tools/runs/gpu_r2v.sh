@@ -6,5 +6,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2v_
 timeout 600 python bench.py > gpurun_out/r2v_bench_c5.json 2> gpurun_out/r2v_bench_c5.err; tail -c 300 gpurun_out/r2v_bench_c5.json
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/r2v_bench_reference.json 2>&1
 timeout 600 python bench.py --workload w26 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r2v_bench_w26.json 2>&1; tail -c 200 gpurun_out/r2v_bench_w26.json
-bash tools/gpu_r2p.sh
+bash tools/runs/gpu_r2p.sh
 cp gpurun_out/r2p_table3_enum.jsonl gpurun_out/r2v_table3_enum.jsonl

@@ -1,6 +1,6 @@
 #!/bin/bash
 # One GPU pass: parity tests, benches, launch list and a full ncu capture of the top kernel.
-# Usage (under gpurun): bash tools/gpu_round.sh <tag> [full]
+# Usage (under gpurun): bash tools/runs/gpu_round.sh <tag> [full]
 TAG=${1:-dev}
 OUT=gpurun_out
 mkdir -p $OUT

@@ -17,6 +17,8 @@ print("enumerate", r.degree, r.cells)
 print("range", p.degree_range(100, 9000).degree)      # mode-0 items
 print("cells", len(p.cells()))
 print("walk", p.degree_walk().degree)                 # start search + k_walk_dc
+V2, w2 = W.c5_points(1, n_points=40, dim=4)           # N > 32: both point slots of the leaf
+print("enumerate N=40", B.Plan.from_points(V2, w2).degree().degree)
 A, b = W.master_space_system(2, 3)
 print("W23", B.degree(A, b).degree, B.Plan.from_system(A, b).degree_walk().degree)
 rng = W.SplitMix64(1)
