@@ -73,6 +73,12 @@ typedef struct {
                                              lies strictly below: no cell); degree,
                                              cells, candidates stay exact, singular becomes an
                                              upper bound (singular_complete = 0)              */
+#define BDEG_FLAG_NATURAL_ORDER     0x80u /* system plans (bdeg_plan): keep the points in first-
+                                             occurrence order.  By default they are sorted by
+                                             ascending lifting (stable) -- the order changes the
+                                             rank space and the work, never a result (DESIGN.md
+                                             reading O); bdeg_plan_points_get returns the order
+                                             in use, and ranks and cell masks refer to it     */
 
 typedef struct {
     uint64_t seed;           /* seed of the generated lifting (and of re-lifts)      */

@@ -144,14 +144,21 @@ def test_master_space_ranges(mk):
     A, b = W.master_space_system(*mk)
     lift = W.liftings(len(A) + 1, 1)
     cfg = point_configuration(A, b, lift)
-    K, V, w = cfg["cone"]
+    # ranks refer to the plan's point order: first occurrence (the oracle's own
+    # configuration, FLAG_NATURAL_ORDER) and the default order sorted by lifting
+    # (the configuration the plan reports, bdeg_plan_points_get)
+    plan_nat = B.Plan.from_system(A, b, lift, flags=B.bdeg.FLAG_NATURAL_ORDER)
     plan = B.Plan.from_system(A, b, lift)
+    K, V, w = cfg["cone"]
+    Kp, Vp, wp = plan.points()
+    assert sorted(wp) == wp and sorted(wp) == sorted(w)
     total = math.comb(len(V), K)
     rng = random.Random(mk[0] * 10 + mk[1])
     for _ in range(6):
         b0 = rng.randrange(0, total - 20000)
         e0 = b0 + rng.randrange(1, 20000)
-        _assert_same(_gpu(plan.degree_range(b0, e0)), enumerate_range(K, V, w, b0, e0, threads=8), (b0, e0))
+        _assert_same(_gpu(plan_nat.degree_range(b0, e0)), enumerate_range(K, V, w, b0, e0, threads=8), (b0, e0))
+        _assert_same(_gpu(plan.degree_range(b0, e0)), enumerate_range(Kp, Vp, wp, b0, e0, threads=8), (b0, e0))
 
 
 def test_table3_degrees_gpu(table3):
@@ -270,8 +277,11 @@ def test_cell_emission_matches_oracle():
     A, b = W.master_space_system(2, 2)
     lift = W.liftings(len(A) + 1, 1)
     K, V, w = point_configuration(A, b, lift)["cone"]
-    got = B.Plan.from_system(A, b, lift).cells()
+    got = B.Plan.from_system(A, b, lift, flags=B.bdeg.FLAG_NATURAL_ORDER).cells()
     assert got == cell_list(K, V, w) and len(got) == 14
+    plan = B.Plan.from_system(A, b, lift)              # default order: masks refer to plan.points()
+    Kp, Vp, wp = plan.points()
+    assert plan.cells() == cell_list(Kp, Vp, wp)
 
 
 @pytest.mark.parametrize("name", ["twisted_cubic", "dp0", "W1_5", "W2_2", "W2_3", "rnc9"])

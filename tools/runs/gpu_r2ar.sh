@@ -1,0 +1,7 @@
+#!/bin/bash
+# round 2, call AR: system plans sorted by lifting -- GPU suite, A/B vs 44f04bc (C5 unchanged: points plan),
+# Table 3 enumeration through the front end
+cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/r2ar_gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r2ar_gpu_tests.log; tail -3 gpurun_out/r2ar_gpu_tests.log
+timeout 1200 bash tools/ab_bench.sh r2ar_liftorder scratch/libbdeg_44f04bc.so -
+timeout 900 bash tools/runs/gpu_r2p.sh > /dev/null 2>&1; cp gpurun_out/r2p_table3_enum.jsonl gpurun_out/r2ar_table3_enum.jsonl; cut -c1-250 gpurun_out/r2ar_table3_enum.jsonl
