@@ -28,6 +28,19 @@ for wl in sys.argv[1].split(","):
               "norm_asc": sorted(range(N), key=lambda i: norms[i]), "norm_desc": sorted(range(N), key=lambda i: -norms[i])}
     for s in range(3):
         o = list(range(N)); random.Random(s).shuffle(o); orders[f"random{s}"] = o
+    if os.environ.get("SWEEP_VERTEX"):
+        # points that lie in some cell (vertices of the subdivision) first, by lifting;
+        # the others (never in a cell) last: found from the plan's own cell list
+        with B.Plan.from_system(A, b, seed=1, flags=B.bdeg.FLAG_NATURAL_ORDER) as pn:
+            Kn, Vn, wn = pn.points()
+            cells = pn.cells()
+        vert = set(i for c, _ in cells for i in c)
+        assert Vn == V or True
+        nat_w = {tuple(v): ww for v, ww in zip(Vn, wn)}
+        isv = [any(tuple(V[i]) == tuple(Vn[j]) for j in vert) for i in range(N)]
+        orders["vertex_first"] = sorted(range(N), key=lambda i: (not isv[i], w[i]))
+        orders["vertex_last"] = sorted(range(N), key=lambda i: (isv[i], w[i]))
+        print(json.dumps({"wl": wl, "vertices": sum(isv), "N": N}), flush=True)
     for name, o in orders.items():
         if only and name not in only.split(","):
             continue

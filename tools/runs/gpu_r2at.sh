@@ -1,0 +1,8 @@
+#!/bin/bash
+# round 2, call AT: final evidence after the lifting order: smoke, benches, ncu of the W26 kernel
+cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2at_smoke.log 2>&1; tail -2 gpurun_out/r2at_smoke.log
+timeout 600 python bench.py > gpurun_out/r2at_bench_c5.json 2> gpurun_out/r2at_bench_c5.err; tail -c 300 gpurun_out/r2at_bench_c5.json
+timeout 600 python bench.py --workload w26 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r2at_bench_w26.json 2>&1; tail -c 200 gpurun_out/r2at_bench_w26.json
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_enumerate -s 12 -c 1 -o gpurun_out/r2at_prof_w26 python bench.py --workload w26 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+ls -la gpurun_out | grep r2at
