@@ -212,7 +212,7 @@ struct Ctx {
     int mytop;           // this lane's entry of the item tuple: c_{kd + lane} (lane < D)
     uint64_t irb, ire;   // the item's candidates n [rank_begin, rank_end)
     bool deg_only;       // skip cell-dead subtrees (singular count becomes an upper bound)
-    bool dead_full;      // full mode: find cell-dead subtrees too (their leaves count singular only)
+    bool dead_full;      // full mode: find cell-dead subtrees too (their leaves only count non-singular j)
     bool partial;        // the item is cut by the rank range
     __device__ __forceinline__ uint64_t C(int n, int k) const { return B[n * kBinomCols + k]; }
     // |[base, base+size) n [irb, ire)| (subtrees below the item level lie inside the item)
@@ -396,7 +396,7 @@ __device__ __forceinline__ void fetch_col(const typename Tr<TIER>::VV (&sv)[NPL]
 // gets multiplied by pivot ratios further down: at any leaf of this subtree
 // the facet test reads sign(g) * y_l with g the node's last pivot.  A
 // negative value means l lies strictly below every hyperplane through the
-// prefix: no cell exists in the subtree (only the singular count remains).
+// prefix: no cell exists in the subtree (only the non-singular count remains).
 template <int TIER, int NPL, int RV>
 __device__ __forceinline__ bool node_dead(const typename Tr<TIER>::VV (&sv)[NPL][RV],
                                           const typename Tr<TIER>::VL (&sl)[NPL], uint64_t inP,
@@ -663,7 +663,7 @@ __device__ __forceinline__ void inner_dfs(const typename Tr<TIER>::VV (&sv)[NPL]
             elim_step<TIER, NPL, RV>(sv, sl, cv, cl, pr, piv, dv, bV, bL, cx, ov, ol, ovf);
             const uint64_t cinP = inP | (1ull << c);
             // cell-dead subtree: degree-only skips it; full mode keeps
-            // walking it for the singular count but its leaves skip the facet test
+            // walking it for the non-singular count but its leaves skip the facet test
             const bool cdead = dead || (cx.dead_full || cx.deg_only) &&
                                            node_dead<TIER, NPL, RV - 1>(ov, ol, cinP, (int64_t)piv, cx);
             if (cdead && cx.deg_only) continue;  // no cell in the subtree: skip it
@@ -748,8 +748,8 @@ __device__ void process_item(int D, int mytop, const int64_t *Lsm, int64_t *scr,
     cx.kd = kd;
     cx.fmin = (D > T) ? kd : S + 1;
     {
-        // effective range = item n [rb, re).  A forced level's subtree spans
-        // other items too: its dependent-prefix count is clamped to [irb, ire).
+        // effective range = item n [rb, re); the item's candidate count is its
+        // size, its singular count |item| - non-singular (Acc).
         const uint64_t rb = cx0.A->rank_begin, re = cx0.A->rank_end;
         const uint64_t lo = tall > rb ? tall : rb;
         const uint64_t hi = tall + isize < re ? tall + isize : re;
