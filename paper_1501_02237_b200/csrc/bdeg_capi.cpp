@@ -229,7 +229,11 @@ void sample_bits(const bdeg_plan_s *p, int &bv, int &bl) {
     i128 mv = 1, ml = 1;
     bool big = false;
     std::vector<int> perm(N);
-    for (int s = 0; s < 32 && !big; ++s) {
+    static const int nsamp = [] {            // tuning knob (A/B of planning time vs tier accuracy)
+        const char *e = std::getenv("BDEG_TIER_SAMPLES");
+        return e ? std::max(1, std::atoi(e)) : 32;
+    }();
+    for (int s = 0; s < nsamp && !big; ++s) {
         for (int i = 0; i < N; ++i) perm[i] = i;
         for (int i = N - 1; i > 0; --i) std::swap(perm[i], perm[g.next() % (uint64_t)(i + 1)]);
         // int64 first (C5, master spaces), checked int128 when a product leaves it
