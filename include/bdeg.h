@@ -147,9 +147,11 @@ bdeg_status bdeg_plan_points(int32_t K, int32_t N, const int64_t *V, const int64
 bdeg_status bdeg_plan_info(bdeg_plan_t plan, bdeg_result *out);
 
 /* The lifted configuration the plan currently enumerates (host copies): V
- * (N*K int64, POINT-major, bdeg_plan_info's point order: distinct non-zero
- * columns of P_0 in variable order, then the origin unless homogeneous —
- * Prop. 4) and omega (N int64: the lifting in use after any
+ * (N*K int64, POINT-major, in the plan's point order — system plans: the
+ * distinct non-zero columns of P_0 and, unless homogeneous, the origin
+ * (Prop. 4), sorted by ascending lifting (or in variable order with
+ * BDEG_FLAG_NATURAL_ORDER); point plans: the caller's order.  Colex ranks,
+ * work items and cell masks refer to this order) and omega (N int64: the lifting in use after any
  * bdeg_relift, and for N > 64 the basis-seeded lifting).  Either
  * pointer may be NULL.  BDEG_E_INVALID for a d = 0 plan (no points). */
 bdeg_status bdeg_plan_points_get(bdeg_plan_t plan, int64_t *V, int64_t *omega);
