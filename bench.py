@@ -59,7 +59,7 @@ class Workload:
             self.lift = W.liftings(len(self.A) + 1, 1)
             self.desc = (f"master space grad W_{{{m},{k}}} (PAPER.md Table 3): x^A = b through the "
                          f"library's front end (n={len(self.A)} variables, m={len(self.A[0])} binomials)")
-            self.extra = {"m": m, "k": k, "seed": 1, "point_order": "ascending lifting (library default for x^A = b plans)"}
+            self.extra = {"m": m, "k": k, "seed": 1, "point_order": "ascending lifting residual (library default for x^A = b plans)"}
         else:
             raise SystemExit(f"unknown workload {name!r} (c5 or w<m><k>)")
 

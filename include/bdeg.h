@@ -75,7 +75,8 @@ typedef struct {
                                              upper bound (singular_complete = 0)              */
 #define BDEG_FLAG_NATURAL_ORDER     0x80u /* system plans (bdeg_plan): keep the points in first-
                                              occurrence order.  By default they are sorted by
-                                             ascending lifting (stable) -- the order changes the
+                                             ascending lifting residual (the lifting minus its
+                                             least-squares linear fit; stable) -- the order changes the
                                              rank space and the work, never a result (DESIGN.md
                                              reading O); bdeg_plan_points_get returns the order
                                              in use, and ranks and cell masks refer to it     */
@@ -149,7 +150,7 @@ bdeg_status bdeg_plan_info(bdeg_plan_t plan, bdeg_result *out);
 /* The lifted configuration the plan currently enumerates (host copies): V
  * (N*K int64, POINT-major, in the plan's point order — system plans: the
  * distinct non-zero columns of P_0 and, unless homogeneous, the origin
- * (Prop. 4), sorted by ascending lifting (or in variable order with
+ * (Prop. 4), sorted by ascending lifting residual (or in variable order with
  * BDEG_FLAG_NATURAL_ORDER); point plans: the caller's order.  Colex ranks,
  * work items and cell masks refer to this order) and omega (N int64: the lifting in use after any
  * bdeg_relift, and for N > 64 the basis-seeded lifting).  Either

@@ -34,7 +34,7 @@ FLAG_FORCE_TIER1 = 0x8
 FLAG_NO_RELIFT = 0x10
 FLAG_FORCE_TIER2 = 0x20
 FLAG_DEGREE_ONLY = 0x40
-FLAG_NATURAL_ORDER = 0x80      # system plans: first-occurrence point order (default: sorted by lifting)
+FLAG_NATURAL_ORDER = 0x80      # system plans: first-occurrence point order (default: sorted by lifting residual)
 TIER_DTYPE = {0: "int32", 1: "int32/int64", 2: "int64/int128", 4: "int128/int256"}
 
 NSLOTS = 16

@@ -682,19 +682,60 @@ bdeg_status finish_plan(bdeg_plan_s *p) {
 
 // rebuild V/w from the current lifting (system plans), in the plan's point
 // order: fixed at planning time as the points sorted by ascending lifting
-// (stable; BDEG_FLAG_NATURAL_ORDER keeps first occurrence).  The order changes
-// which K-subsets share prefixes, never a result (reading O); measured on the
-// master spaces (profiles/r2aq_order_sweep.jsonl) it is the fastest of the
-// orders tried: W_{2,6} -11 %, W_{2,7} -15 %, W_{3,5} / W_{4,4} degree-only
-// -17 % / -12 % against first occurrence.  Re-lifts keep the order.
+// residual (the lifting minus its least-squares linear fit; stable;
+// BDEG_FLAG_NATURAL_ORDER keeps first occurrence).  High points are fixed
+// first by the colex DFS, so cell-dead prefixes are found higher up.  The
+// order changes which K-subsets share prefixes, never a result (reading O);
+// measured on the master spaces (profiles/r2aq/r2az_order_sweep.jsonl) against
+// first occurrence: W_{2,6} -15 %, W_{2,5} -23 %, W_{2,7} -13 %, W_{3,5} and
+// W_{4,4} degree-only -17 % and -12 %.  Re-lifts keep the order.
 void rebuild_points(bdeg_plan_s *p) {
     build_points(p->fe, p->lift.data(), !(p->opt.flags & BDEG_FLAG_NO_HOMOG_SHORTCUT), p->K, p->N, p->V,
                  p->w, p->point_of_var, p->origin_index);
     if (p->opt.flags & BDEG_FLAG_NATURAL_ORDER) return;
     if ((int)p->order.size() != p->N) {
-        p->order.resize(p->N);
-        for (int l = 0; l < p->N; ++l) p->order[l] = l;
-        std::stable_sort(p->order.begin(), p->order.end(), [&](int a, int b) { return p->w[a] < p->w[b]; });
+        // sort key: the lifting minus its least-squares linear fit (normal
+        // equations in double; only an order, so rounding is harmless) -- adding
+        // a linear function to the lifting changes neither the subdivision nor
+        // this key (the raw lifting would be ordered by the added function)
+        const int K = p->K, N = p->N;
+        std::vector<double> G((size_t)K * K, 0.0), r(K, 0.0), h(K, 0.0), key(N);
+        for (int l = 0; l < N; ++l)
+            for (int i = 0; i < K; ++i) {
+                const double vi = (double)p->V[(size_t)l * K + i];
+                r[i] += vi * (double)p->w[l];
+                for (int j = 0; j < K; ++j) G[(size_t)i * K + j] += vi * (double)p->V[(size_t)l * K + j];
+            }
+        bool ok = true;                        // Gaussian elimination with partial pivoting
+        for (int c = 0; c < K && ok; ++c) {
+            int piv = c;
+            for (int i = c + 1; i < K; ++i)
+                if (std::fabs(G[(size_t)i * K + c]) > std::fabs(G[(size_t)piv * K + c])) piv = i;
+            if (std::fabs(G[(size_t)piv * K + c]) < 1e-300) { ok = false; break; }
+            if (piv != c) {
+                for (int j = 0; j < K; ++j) std::swap(G[(size_t)c * K + j], G[(size_t)piv * K + j]);
+                std::swap(r[c], r[piv]);
+            }
+            for (int i = c + 1; i < K; ++i) {
+                const double f = G[(size_t)i * K + c] / G[(size_t)c * K + c];
+                for (int j = c; j < K; ++j) G[(size_t)i * K + j] -= f * G[(size_t)c * K + j];
+                r[i] -= f * r[c];
+            }
+        }
+        for (int c = K - 1; c >= 0 && ok; --c) {
+            double t = r[c];
+            for (int j = c + 1; j < K; ++j) t -= G[(size_t)c * K + j] * h[j];
+            h[c] = t / G[(size_t)c * K + c];
+        }
+        for (int l = 0; l < N; ++l) {
+            double fit = 0;
+            if (ok)
+                for (int i = 0; i < K; ++i) fit += h[i] * (double)p->V[(size_t)l * K + i];
+            key[l] = (double)p->w[l] - fit;
+        }
+        p->order.resize(N);
+        for (int l = 0; l < N; ++l) p->order[l] = l;
+        std::stable_sort(p->order.begin(), p->order.end(), [&](int a, int b) { return key[a] < key[b]; });
     }
     std::vector<int64_t> V2((size_t)p->N * p->K), w2(p->N);
     std::vector<int> pos(p->N);

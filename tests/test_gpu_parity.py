@@ -146,12 +146,12 @@ def test_master_space_ranges(mk):
     cfg = point_configuration(A, b, lift)
     # ranks refer to the plan's point order: first occurrence (the oracle's own
     # configuration, FLAG_NATURAL_ORDER) and the default order sorted by lifting
-    # (the configuration the plan reports, bdeg_plan_points_get)
+    # residual (the configuration the plan reports, bdeg_plan_points_get)
     plan_nat = B.Plan.from_system(A, b, lift, flags=B.bdeg.FLAG_NATURAL_ORDER)
     plan = B.Plan.from_system(A, b, lift)
     K, V, w = cfg["cone"]
     Kp, Vp, wp = plan.points()
-    assert sorted(wp) == wp and sorted(wp) == sorted(w)
+    assert sorted(wp) == sorted(w)                     # the same points, the plan's order
     total = math.comb(len(V), K)
     rng = random.Random(mk[0] * 10 + mk[1])
     for _ in range(6):

@@ -28,6 +28,12 @@ for wl in sys.argv[1].split(","):
               "norm_asc": sorted(range(N), key=lambda i: norms[i]), "norm_desc": sorted(range(N), key=lambda i: -norms[i])}
     for s in range(3):
         o = list(range(N)); random.Random(s).shuffle(o); orders[f"random{s}"] = o
+    # lifting minus its least-squares linear fit (invariant under adding a linear function)
+    import numpy as np
+    Vm = np.array(V, dtype=np.float64); wv = np.array(w, dtype=np.float64)
+    h = np.linalg.lstsq(Vm, wv, rcond=None)[0]
+    res = wv - Vm @ h
+    orders["resid_asc"] = sorted(range(N), key=lambda i: res[i])
     if os.environ.get("SWEEP_VERTEX"):
         # points that lie in some cell (vertices of the subdivision) first, by lifting;
         # the others (never in a cell) last: found from the plan's own cell list
